@@ -99,14 +99,17 @@ edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, co
                          float* table, void* saved, void* stream);
 
 /* F2 -- reconstruct this rank's slice of each tensor (Fig. 1, "look-up").
+ *   table, C_out : the outputs of edkm_forward (table is read only by EDKM_SOFT with
+ *                  FP32 output, C_out only by EDKM_HARD_VALUE; the other may be NULL).
  *   out[t] : n_t elements of out_dtype.
  *   EDKM_SOFT:        out_dtype FP32 (table entry), or the weights' own 16-bit dtype
  *                     (round-to-nearest-even from the fp64 value).
  *   EDKM_HARD_VALUE:  out_dtype FP32 or the weights' 16-bit dtype; value C_out[idx].
  *   EDKM_HARD_INDEX:  out_dtype U8; idx = argmin_j (v - C_out[j])^2, lowest j on ties,
  *                     distances in fp64 from the fp32 C_out values (DESIGN R9). */
-edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* saved,
-                             int mode, int out_dtype, void* const* out, void* stream);
+edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_params* p, const float* table,
+                             const float* C_out, const void* saved, int mode, int out_dtype, void* const* out,
+                             void* stream);
 
 /* B1 -- gradient buckets and this rank's partial of gamma_T (DESIGN App. A):
  *   B[u] = sum_{i in slice, bits(w_i)=u} G_i  (64-bit fixed point per CTA, fp64 across CTAs)

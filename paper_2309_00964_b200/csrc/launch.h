@@ -1,0 +1,78 @@
+// launch.h -- internal launcher declarations shared by the .cu files of libedkm.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace edkm {
+
+// ---- per-tensor forward state kept in `saved`
+constexpr int kMaxCluster = 8;
+struct TensorState {
+  int32_t T;                       // centroid updates run
+  int32_t cl;                      // CTAs per tensor in the table phase (row partitions)
+  int64_t nonfinite[kMaxCluster];  // NaN/Inf weights counted, per partition
+  int32_t nrows[kMaxCluster];      // populated finite patterns, per partition
+  int32_t pad[6];
+};
+static_assert(sizeof(TensorState) == 128, "TensorState layout");
+
+struct SavedLayout {
+  size_t state, ctraj, straj, rows, table16, idx8, page_cnt, total;
+};
+struct WsLayout {
+  size_t B, psi, phipsi, gamma, total;
+};
+SavedLayout saved_layout(int nt, int k, int max_iter);
+WsLayout ws_layout(int nt, int k);
+
+// F2 mode: 0 soft 16-bit, 1 hard-value 16-bit, 2 soft fp32, 3 hard-value fp32, 4 hard index u8
+struct F2Args {
+  const float* table;       // [nt][65536] fp32 W~ per pattern
+  const uint16_t* table16;  // [nt][65536] W~ rounded to the weights' dtype
+  const uint8_t* idx8;      // [nt][65536] hard index per pattern
+  const float* C;           // [nt][k] C_out
+  const int64_t* page_cnt;  // [nt][256]
+  int k;
+};
+struct B1Args {
+  double* B;                // [nt][65536] fp64, zeroed by the caller
+  const int64_t* page_cnt;  // [nt][256]
+};
+struct B2Args {
+  const float2* phipsi;     // [nt][65536] (phi, psi) per pattern
+  const int64_t* page_cnt;  // [nt][256]
+};
+cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s);
+cudaError_t launch_f2(const StreamArgs& A, const F2Args& F, int mode, int sms, cudaStream_t s);
+cudaError_t launch_b1(const StreamArgs& A, const B1Args& B, int sms, cudaStream_t s);
+cudaError_t launch_b2(const StreamArgs& A, const B2Args& B, int sms, cudaStream_t s);
+
+// ---- table phase
+struct TableArgs {
+  int nt, k, wdtype, max_iter, cl;
+  double tau, inv_tau, eps;
+  const int32_t* counts;   // [nt][65536]
+  const float* C0;         // [nt][k]
+  float* C_out;            // [nt][k]
+  float* table;            // [nt][65536]
+  TensorState* state;      // [nt]
+  double* ctraj;           // [nt][(max_iter+1)*k]
+  double* straj;           // [nt][max(max_iter,1)*k]
+  uint16_t* rows;          // [nt][65536] populated finite patterns, by partition
+  uint16_t* table16;       // [nt][65536]
+  uint8_t* idx8;           // [nt][65536]
+  int64_t* page_cnt;       // [nt][256]
+  const double* B;         // [nt][65536] gradient buckets
+  double* psi;             // [nt][65536] per-row psi accumulator
+  float2* phipsi;          // [nt][65536]
+  double* gamma;           // [nt][k]
+  float* dC0;              // [nt][k]
+};
+int table_cluster_size(int nt);
+cudaError_t launch_tf(const TableArgs& P, cudaStream_t s);
+cudaError_t launch_tgamma(const TableArgs& P, cudaStream_t s);
+cudaError_t launch_tb(const TableArgs& P, cudaStream_t s);
+
+}  // namespace edkm

@@ -1,0 +1,491 @@
+// stream_kernels.cu -- the four per-weight passes of the eDKM hot path (S3).
+//
+//   F1  uniquify: counts[u] = #{i : bits(w_i) = u}            (Fig. 3)
+//   F2  reconstruct: W~_i = table[bits(w_i)] (or hard modes)    (Fig. 1, "look-up")
+//   B1  gradient buckets: B[u] = sum_{bits(w_i)=u} G_i          (DESIGN App. A)
+//   B2  dW_i = G_i phi[bits(w_i)] + psi[bits(w_i)]               (DESIGN App. A)
+//
+// All four are HBM-streaming kernels: persistent grid (one 1024-thread CTA per
+// SM, its shared memory holding one tensor's per-pattern table), a static
+// contiguous split of the concatenated weight space, 256-bit evict-first loads,
+// and the per-pattern table in shared memory.  No tensor cores: nothing here
+// is a contraction.
+#include "common.cuh"
+#include "launch.h"
+
+namespace edkm {
+
+constexpr int kThreads = 1024;   // F1, F2
+constexpr int kThreadsB = 512;   // B1, B2: two inputs per element need more registers
+constexpr int kF1Bins = 57344;  // patterns < 0xE000 counted in SMEM (224 KiB); the rest in L2
+constexpr int kB1Pages = 55;    // magnitude pages per sign kept by B1 (8 B/pattern)
+constexpr int kB2Pages = 55;    // B2 (float2 phi, psi)
+constexpr int kF2Pages32 = 110; // F2 fp32 output (4 B/pattern)
+
+// ----------------------------------------------------------------------------
+// Generic visitor over this CTA's slice of the concatenated tensors.
+// P::Vec is the register payload of one 16-element vector; vectors are
+// processed two at a time so each thread keeps 2 x 32 B (or more) in flight.
+// ----------------------------------------------------------------------------
+template <class P>
+__device__ __forceinline__ void for_each_segment(const StreamArgs& A, P& p) {
+  int64_t lo, hi;
+  cta_range(A.total, lo, hi);
+  if (lo >= hi) return;
+  int t = find_tensor(A, lo);
+  const int tid = threadIdx.x, bs = blockDim.x;
+  while (lo < hi) {
+    while (A.offs[t + 1] <= lo) ++t;
+    const int64_t a = lo - A.offs[t], b = min(hi, A.offs[t + 1]) - A.offs[t];
+    p.begin(t, a, b);
+    const uintptr_t wa = (uintptr_t)(A.w[t] + a);
+    int64_t head = min((int64_t)(((32u - (uint32_t)(wa & 31u)) & 31u) >> 1), b - a);
+    const int64_t va = a + head;
+    int64_t nv = (b - va) >> 4;
+    if (nv > 0 && !p.vec_ok(t, va)) { head = b - a; nv = 0; }
+    for (int64_t i = a + tid; i < a + head; i += bs) p.scalar(t, i);
+    int64_t v = tid;
+    for (; v + bs < nv; v += 2 * bs) {
+      typename P::Vec r0, r1;
+      p.load(t, va + 16 * v, r0);
+      p.load(t, va + 16 * (v + bs), r1);
+      p.process(t, va + 16 * v, r0);
+      p.process(t, va + 16 * (v + bs), r1);
+    }
+    if (v < nv) {
+      typename P::Vec r0;
+      p.load(t, va + 16 * v, r0);
+      p.process(t, va + 16 * v, r0);
+    }
+    for (int64_t i = va + 16 * nv + tid; i < b; i += bs) p.scalar(t, i);
+    p.end(t);
+    lo = A.offs[t] + b;
+    ++t;
+  }
+}
+
+__device__ __forceinline__ uint32_t pat(const V8& v, int e) { return (v.x[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu; }
+
+// ============================================================================ F1
+struct F1Policy {
+  const StreamArgs& A;
+  uint32_t* h;
+  int32_t* counts;  // [nt_total][65536], this launch's tensors start at t0
+  struct Vec { V8 w; };
+  __device__ int32_t* cnt(int t) const { return counts + (int64_t)(A.t0 + t) * kPatterns; }
+  __device__ void begin(int, int64_t, int64_t) {
+    uint4* h4 = reinterpret_cast<uint4*>(h);
+    for (int i = threadIdx.x; i < kF1Bins / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
+  __device__ bool vec_ok(int, int64_t) const { return true; }
+  __device__ void load(int t, int64_t i, Vec& r) const { r.w = ldg_stream8(A.w[t] + i); }
+  __device__ void count(int t, uint32_t u) {
+    if (u < (uint32_t)kF1Bins) red_shared_add(&h[u], 1u);
+    else atomicAdd(&cnt(t)[u], 1);
+  }
+  __device__ void process(int t, int64_t, const Vec& r) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) count(t, pat(r.w, e));
+  }
+  __device__ void scalar(int t, int64_t i) { count(t, A.w[t][i]); }
+  __device__ void end(int t) {
+    __syncthreads();
+    int32_t* c = cnt(t);
+    for (int i = threadIdx.x; i < kF1Bins; i += blockDim.x) {
+      const uint32_t v = h[i];
+      if (v) atomicAdd(&c[i], (int32_t)v);
+    }
+    __syncthreads();
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_constant__ StreamArgs A, int32_t* counts) {
+  extern __shared__ __align__(16) uint32_t smem_u32[];
+  F1Policy p{A, smem_u32, counts};
+  for_each_segment(A, p);
+}
+
+// ============================================================================ F2
+// mode: 0 soft 16-bit, 1 hard-value 16-bit, 2 soft fp32, 3 hard-value fp32, 4 hard index u8
+
+
+template <int MODE>
+struct F2Policy {
+  const StreamArgs& A;
+  const F2Args& F;
+  unsigned char* sm;
+  int pbase, np;
+  struct Vec { V8 w; };
+  __device__ int gt(int t) const { return A.t0 + t; }
+  __device__ void begin(int t, int64_t, int64_t) {
+    const int T = gt(t);
+    if (MODE == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(F.table16 + (int64_t)T * kPatterns);
+      uint4* dst = reinterpret_cast<uint4*>(sm);
+      for (int i = threadIdx.x; i < kPatterns * 2 / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    } else if (MODE == 1) {
+      uint16_t* tab = reinterpret_cast<uint16_t*>(sm);
+      const uint8_t* ix = F.idx8 + (int64_t)T * kPatterns;
+      const float* C = F.C + (int64_t)T * F.k;
+      for (int u = threadIdx.x; u < kPatterns; u += blockDim.x)
+        tab[u] = pattern_finite(u, A.wdtype) ? round16f(__ldg(C + ix[u]), A.wdtype) : nan16(A.wdtype);
+    } else if (MODE == 2) {
+      __shared__ int s_w[2];
+      if (threadIdx.x < 32) choose_window(F.page_cnt + (int64_t)T * 256, kF2Pages32, &s_w[0], &s_w[1]);
+      __syncthreads();
+      pbase = s_w[0];
+      np = s_w[1];
+      float* tab = reinterpret_cast<float*>(sm);
+      const float* src = F.table + (int64_t)T * kPatterns;
+      for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
+    } else {
+      uint8_t* ix = reinterpret_cast<uint8_t*>(sm);
+      const uint4* src = reinterpret_cast<const uint4*>(F.idx8 + (int64_t)T * kPatterns);
+      uint4* dst = reinterpret_cast<uint4*>(ix);
+      for (int i = threadIdx.x; i < kPatterns / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+      if (MODE == 3) {
+        float* Cs = reinterpret_cast<float*>(sm + kPatterns);
+        if (threadIdx.x < F.k) Cs[threadIdx.x] = F.C[(int64_t)T * F.k + threadIdx.x];
+      }
+    }
+    __syncthreads();
+  }
+  __device__ bool vec_ok(int t, int64_t i) const {
+    const int osz = (MODE == 0 || MODE == 1) ? 2 : (MODE == 4 ? 1 : 4);
+    const uintptr_t o = (uintptr_t)A.out[t] + (uintptr_t)i * osz;
+    return (o & (MODE == 4 ? 15u : 31u)) == 0;
+  }
+  __device__ void load(int t, int64_t i, Vec& r) const { r.w = ldg_stream8(A.w[t] + i); }
+  __device__ float f32_of(int t, uint32_t u) const {
+    if (MODE == 2) {
+      const int s = window_slot(u, pbase, np);
+      return s >= 0 ? reinterpret_cast<const float*>(sm)[s] : __ldg(F.table + (int64_t)gt(t) * kPatterns + u);
+    }
+    // MODE 3: non-finite patterns have NaN value
+    if (!pattern_finite(u, A.wdtype)) return __int_as_float(0x7FC00000);
+    return reinterpret_cast<const float*>(sm + kPatterns)[sm[u]];
+  }
+  __device__ void process(int t, int64_t i, const Vec& r) {
+    if (MODE == 0 || MODE == 1) {
+      const uint16_t* tab = reinterpret_cast<const uint16_t*>(sm);
+      V8 o;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o.x[q] = (uint32_t)tab[r.w.x[q] & 0xFFFFu] | ((uint32_t)tab[r.w.x[q] >> 16] << 16);
+      stg_stream8(reinterpret_cast<uint16_t*>(A.out[t]) + i, o);
+    } else if (MODE == 2 || MODE == 3) {
+      V8 o0, o1;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o0.x[e] = __float_as_uint(f32_of(t, pat(r.w, e)));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o1.x[e] = __float_as_uint(f32_of(t, pat(r.w, 8 + e)));
+      float* out = reinterpret_cast<float*>(A.out[t]) + i;
+      stg_stream8(out, o0);
+      stg_stream8(out + 8, o1);
+    } else {
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t a = r.w.x[2 * q], b = r.w.x[2 * q + 1];
+        o[q] = (uint32_t)sm[a & 0xFFFFu] | ((uint32_t)sm[a >> 16] << 8) | ((uint32_t)sm[b & 0xFFFFu] << 16) |
+               ((uint32_t)sm[b >> 16] << 24);
+      }
+      stg_stream4(reinterpret_cast<uint8_t*>(A.out[t]) + i, o[0], o[1], o[2], o[3]);
+    }
+  }
+  __device__ void scalar(int t, int64_t i) {
+    const uint32_t u = A.w[t][i];
+    if (MODE == 0 || MODE == 1) reinterpret_cast<uint16_t*>(A.out[t])[i] = reinterpret_cast<const uint16_t*>(sm)[u];
+    else if (MODE == 2 || MODE == 3) reinterpret_cast<float*>(A.out[t])[i] = f32_of(t, u);
+    else reinterpret_cast<uint8_t*>(A.out[t])[i] = sm[u];
+  }
+  __device__ void end(int) { __syncthreads(); }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_constant__ StreamArgs A, const F2Args F) {
+  extern __shared__ __align__(16) unsigned char smem_u8[];
+  F2Policy<MODE> p{A, F, smem_u8, 0, 0};
+  for_each_segment(A, p);
+}
+
+// ============================================================================ B1
+// B[u] = sum G_i over this CTA's weights with pattern u, accumulated exactly in
+// 64-bit fixed point (lo: u32, hi: i32) with native shared-memory integer
+// atomics -- sm_100 has no native shared fp32 atomic add (it is a CAS loop).
+// The per-segment scale 2^s maps the largest |G| of a 16K-element sample to
+// [2^27, 2^28); an element whose |q| would reach 2^31, or any non-finite G,
+// goes straight to the fp64 global bucket (correct, slower).  The exact
+// per-CTA sum is converted to fp64 once and added to the global bucket.
+
+
+template <int GF32>
+struct B1Policy {
+  const StreamArgs& A;
+  const B1Args& Bq;
+  uint32_t* lo;
+  int32_t* hi;
+  int pbase, np;
+  float scale;  // 2^s
+  double inv_scale;
+  bool active;  // scale established (some finite nonzero G)
+  struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
+  __device__ double* bucket(int t) const { return Bq.B + (int64_t)(A.t0 + t) * kPatterns; }
+  __device__ float gval(int t, int64_t i) const {
+    if (GF32) return reinterpret_cast<const float*>(A.g[t])[i];
+    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], A.gdtype);
+  }
+  __device__ void begin(int t, int64_t a, int64_t b) {
+    __shared__ int s_w[2];
+    __shared__ unsigned s_max;
+    if (threadIdx.x == 0) s_max = 0;
+    if (threadIdx.x < 32) choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB1Pages, &s_w[0], &s_w[1]);
+    __syncthreads();
+    pbase = s_w[0];
+    np = s_w[1];
+    uint4* z = reinterpret_cast<uint4*>(lo);
+    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) z[s] = make_uint4(0, 0, 0, 0);
+    uint4* zh = reinterpret_cast<uint4*>(hi);
+    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) zh[s] = make_uint4(0, 0, 0, 0);
+    // scale from the max finite |G| of a sample (whole segment if the sample is all zero)
+    unsigned m = 0;
+    const int64_t sample_end = min(b, a + 16384);
+    for (int pass = 0; pass < 2; ++pass) {
+      const int64_t e_end = pass == 0 ? sample_end : b;
+      for (int64_t i = (pass == 0 ? a : sample_end) + threadIdx.x; i < e_end; i += blockDim.x) {
+        const unsigned ab = __float_as_uint(fabsf(gval(t, i)));
+        if (ab < 0x7F800000u) m = max(m, ab);
+      }
+      m = __reduce_max_sync(0xffffffffu, m);
+      if ((threadIdx.x & 31) == 0) atomicMax(&s_max, m);
+      __syncthreads();
+      if (s_max != 0) break;
+      __syncthreads();
+    }
+    const unsigned mx = s_max;
+    active = false;
+    if (mx != 0) {
+      int e;
+      frexpf(__uint_as_float(mx), &e);  // mx in [2^(e-1), 2^e)
+      const int s = 28 - e;              // mx * 2^s in [2^27, 2^28)
+      if (s <= 126 && s >= -126) {
+        active = true;
+        scale = ldexpf(1.0f, s);
+        inv_scale = ldexp(1.0, -s);
+      }
+    }
+    __syncthreads();
+  }
+  __device__ bool vec_ok(int t, int64_t i) const {
+    const uintptr_t g = (uintptr_t)A.g[t] + (uintptr_t)i * (GF32 ? 4 : 2);
+    return (g & 31u) == 0;
+  }
+  __device__ void load(int t, int64_t i, Vec& r) const {
+    r.w = ldg_stream8(A.w[t] + i);
+    if (GF32) {
+      r.g[0] = ldg_stream8(reinterpret_cast<const float*>(A.g[t]) + i);
+      r.g[GF32] = ldg_stream8(reinterpret_cast<const float*>(A.g[t]) + i + 8);
+    } else {
+      r.g[0] = ldg_stream8(reinterpret_cast<const uint16_t*>(A.g[t]) + i);
+    }
+  }
+  __device__ __forceinline__ void add(int t, uint32_t u, float g) {
+    const float x = g * scale;
+    const int slot = window_slot(u, pbase, np);
+    if (active && slot >= 0 && fabsf(x) < 2147483520.0f) {
+      const int q = __float2int_rn(x);
+      const uint32_t add = (uint32_t)q;
+      const uint32_t old = atomicAdd(&lo[slot], add);
+      const int delta = (int)(old + add < old) - (int)(q < 0);
+      if (delta) atomicAdd(&hi[slot], delta);
+    } else if (g != 0.0f) {
+      atomicAdd(&bucket(t)[u], (double)g);
+    }
+  }
+  __device__ void process(int t, int64_t, const Vec& r) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      float g;
+      if (GF32) g = __uint_as_float(r.g[e >> 3].x[e & 7]);
+      else g = decode16f(pat(r.g[0], e), A.gdtype);
+      add(t, pat(r.w, e), g);
+    }
+  }
+  __device__ void scalar(int t, int64_t i) { add(t, A.w[t][i], gval(t, i)); }
+  __device__ void end(int t) {
+    __syncthreads();
+    if (active) {
+      double* Bt = bucket(t);
+      for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) {
+        const int64_t v = ((int64_t)hi[s] << 32) + (int64_t)lo[s];
+        if (v != 0) atomicAdd(&Bt[slot_pattern(s, pbase, np)], (double)v * inv_scale);
+      }
+    }
+    __syncthreads();
+  }
+};
+
+template <int GF32>
+__global__ void __launch_bounds__(kThreadsB, 1) b1_bucket_kernel(const __grid_constant__ StreamArgs A, const B1Args Bq) {
+  extern __shared__ __align__(16) uint32_t smem_b1[];
+  B1Policy<GF32> p{A, Bq, smem_b1, reinterpret_cast<int32_t*>(smem_b1 + 2 * kB1Pages * 256), 0, 0, 0.f, 0.0, false};
+  for_each_segment(A, p);
+}
+
+// ============================================================================ B2
+
+
+template <int GF32, int OF32>
+struct B2Policy {
+  const StreamArgs& A;
+  const B2Args& Bq;
+  float2* tab;
+  int pbase, np;
+  struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
+  __device__ const float2* glob(int t) const { return Bq.phipsi + (int64_t)(A.t0 + t) * kPatterns; }
+  __device__ float gval(int t, int64_t i) const {
+    if (GF32) return reinterpret_cast<const float*>(A.g[t])[i];
+    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], A.gdtype);
+  }
+  __device__ void begin(int t, int64_t, int64_t) {
+    __shared__ int s_w[2];
+    if (threadIdx.x < 32) choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB2Pages, &s_w[0], &s_w[1]);
+    __syncthreads();
+    pbase = s_w[0];
+    np = s_w[1];
+    const float2* src = glob(t);
+    for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
+    __syncthreads();
+  }
+  __device__ bool vec_ok(int t, int64_t i) const {
+    const uintptr_t g = (uintptr_t)A.g[t] + (uintptr_t)i * (GF32 ? 4 : 2);
+    const uintptr_t o = (uintptr_t)A.out[t] + (uintptr_t)i * (OF32 ? 4 : 2);
+    return ((g | o) & 31u) == 0;
+  }
+  __device__ void load(int t, int64_t i, Vec& r) const {
+    r.w = ldg_stream8(A.w[t] + i);
+    if (GF32) {
+      r.g[0] = ldg_stream8(reinterpret_cast<const float*>(A.g[t]) + i);
+      r.g[GF32] = ldg_stream8(reinterpret_cast<const float*>(A.g[t]) + i + 8);
+    } else {
+      r.g[0] = ldg_stream8(reinterpret_cast<const uint16_t*>(A.g[t]) + i);
+    }
+  }
+  __device__ __forceinline__ float dw(int t, uint32_t u, float g) const {
+    const int s = window_slot(u, pbase, np);
+    const float2 pp = s >= 0 ? tab[s] : __ldg(glob(t) + u);
+    return fmaf(g, pp.x, pp.y);
+  }
+  __device__ void process(int t, int64_t i, const Vec& r) {
+    float d[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      float g;
+      if (GF32) g = __uint_as_float(r.g[e >> 3].x[e & 7]);
+      else g = decode16f(pat(r.g[0], e), A.gdtype);
+      d[e] = dw(t, pat(r.w, e), g);
+    }
+    if (OF32) {
+      V8 o0, o1;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { o0.x[e] = __float_as_uint(d[e]); o1.x[e] = __float_as_uint(d[8 + e]); }
+      float* out = reinterpret_cast<float*>(A.out[t]) + i;
+      stg_stream8(out, o0);
+      stg_stream8(out + 8, o1);
+    } else {
+      V8 o;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        o.x[q] = (uint32_t)round16f(d[2 * q], A.wdtype) | ((uint32_t)round16f(d[2 * q + 1], A.wdtype) << 16);
+      stg_stream8(reinterpret_cast<uint16_t*>(A.out[t]) + i, o);
+    }
+  }
+  __device__ void scalar(int t, int64_t i) {
+    const float d = dw(t, A.w[t][i], gval(t, i));
+    if (OF32) reinterpret_cast<float*>(A.out[t])[i] = d;
+    else reinterpret_cast<uint16_t*>(A.out[t])[i] = round16f(d, A.wdtype);
+  }
+  __device__ void end(int) { __syncthreads(); }
+};
+
+template <int GF32, int OF32>
+__global__ void __launch_bounds__(kThreadsB, 1) b2_dw_kernel(const __grid_constant__ StreamArgs A, const B2Args Bq) {
+  extern __shared__ __align__(16) float2 smem_b2[];
+  B2Policy<GF32, OF32> p{A, Bq, smem_b2, 0, 0};
+  for_each_segment(A, p);
+}
+
+// ============================================================================ launchers
+static int grid_for(int64_t total, int sms) {
+  int64_t g = (total + 16383) / 16384;
+  if (g > sms) g = sms;
+  return g < 1 ? 1 : (int)g;
+}
+
+static cudaError_t set_smem(const void* fn, size_t bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s) {
+  if (A.total == 0) return cudaSuccess;
+  const size_t smem = kF1Bins * sizeof(uint32_t);
+  cudaError_t e = set_smem((const void*)f1_hist_kernel, smem);
+  if (e != cudaSuccess) return e;
+  f1_hist_kernel<<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f2(const StreamArgs& A, const F2Args& F, int mode, int sms, cudaStream_t s) {
+  if (A.total == 0) return cudaSuccess;
+  const void* fn;
+  size_t smem;
+  switch (mode) {
+    case 0: fn = (const void*)f2_gather_kernel<0>; smem = kPatterns * 2; break;
+    case 1: fn = (const void*)f2_gather_kernel<1>; smem = kPatterns * 2; break;
+    case 2: fn = (const void*)f2_gather_kernel<2>; smem = 2 * kF2Pages32 * 256 * 4; break;
+    case 3: fn = (const void*)f2_gather_kernel<3>; smem = kPatterns + 256 * 4; break;
+    default: fn = (const void*)f2_gather_kernel<4>; smem = kPatterns; break;
+  }
+  cudaError_t e = set_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const int g = grid_for(A.total, sms);
+  switch (mode) {
+    case 0: f2_gather_kernel<0><<<g, kThreads, smem, s>>>(A, F); break;
+    case 1: f2_gather_kernel<1><<<g, kThreads, smem, s>>>(A, F); break;
+    case 2: f2_gather_kernel<2><<<g, kThreads, smem, s>>>(A, F); break;
+    case 3: f2_gather_kernel<3><<<g, kThreads, smem, s>>>(A, F); break;
+    default: f2_gather_kernel<4><<<g, kThreads, smem, s>>>(A, F); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_b1(const StreamArgs& A, const B1Args& Bq, int sms, cudaStream_t s) {
+  if (A.total == 0) return cudaSuccess;
+  const size_t smem = 2 * kB1Pages * 256 * 8;
+  const bool f32 = A.gdtype == kFP32;
+  const void* fn = f32 ? (const void*)b1_bucket_kernel<1> : (const void*)b1_bucket_kernel<0>;
+  cudaError_t e = set_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const int g = grid_for(A.total, sms);
+  if (f32) b1_bucket_kernel<1><<<g, kThreadsB, smem, s>>>(A, Bq);
+  else b1_bucket_kernel<0><<<g, kThreadsB, smem, s>>>(A, Bq);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_b2(const StreamArgs& A, const B2Args& Bq, int sms, cudaStream_t s) {
+  if (A.total == 0) return cudaSuccess;
+  const size_t smem = 2 * kB2Pages * 256 * 8;
+  const int gf = A.gdtype == kFP32, of = A.odtype == kFP32;
+  const void* fn = gf ? (of ? (const void*)b2_dw_kernel<1, 1> : (const void*)b2_dw_kernel<1, 0>)
+                      : (of ? (const void*)b2_dw_kernel<0, 1> : (const void*)b2_dw_kernel<0, 0>);
+  cudaError_t e = set_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const int g = grid_for(A.total, sms);
+  if (gf && of) b2_dw_kernel<1, 1><<<g, kThreadsB, smem, s>>>(A, Bq);
+  else if (gf) b2_dw_kernel<1, 0><<<g, kThreadsB, smem, s>>>(A, Bq);
+  else if (of) b2_dw_kernel<0, 1><<<g, kThreadsB, smem, s>>>(A, Bq);
+  else b2_dw_kernel<0, 0><<<g, kThreadsB, smem, s>>>(A, Bq);
+  return cudaGetLastError();
+}
+
+}  // namespace edkm

@@ -1,0 +1,358 @@
+"""Thin Python binding of libedkm.so (include/edkm.h) -- argument marshalling only.
+
+Every step of the eDKM hot path runs in the CUDA kernels behind the C ABI; this
+module turns torch tensors into raw device pointers and the current CUDA stream
+into a ``cudaStream_t``.  There is no CPU fallback: if libedkm.so is missing or
+a call fails, an exception is raised.
+
+Entry points (same names as the C ABI; PAPER.md = /root/reference/PAPER.md):
+  uniquify          F1: counts per 16-bit pattern (Fig. 3)
+  forward           TF: unrolled DKM iterations on the attention table
+  reconstruct       F2: W~ = table[bits(w)] / hard palettisation (Fig. 1)
+  backward_reduce   B1 + gamma_T partial
+  backward_apply    TB + B2: dC_0 and dW
+  backward          both (single process)
+``Plan`` owns the per-step buffers (counts, saved, ws, ...) so a training step
+allocates nothing; ``EDKMFunction`` wraps one tensor as a torch.autograd.Function.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libedkm.so")
+
+BF16, FP16, FP32, U8 = 0, 1, 2, 3
+SOFT, HARD_VALUE, HARD_INDEX = 0, 1, 2
+PATTERNS = 65536
+
+_DT = {torch.bfloat16: BF16, torch.float16: FP16, torch.float32: FP32, torch.uint8: U8}
+
+
+class EDKMError(RuntimeError):
+    pass
+
+
+class _Tensor(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("wdtype", ctypes.c_int), ("bits", ctypes.c_int), ("tau", ctypes.c_double),
+                ("max_iter", ctypes.c_int), ("eps", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libedkm.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EDKMError(f"{LIB_PATH} not found: run `python -m paper_2309_00964_b200.build` "
+                            "(or __graft_entry__.build()) first")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+        pp = ctypes.POINTER(_Params)
+        sig = {
+            "edkm_saved_bytes": ([i32, pp], ctypes.c_size_t),
+            "edkm_workspace_bytes": ([i32, pp], ctypes.c_size_t),
+            "edkm_uniquify": ([P, i32, i32, P, P], i32),
+            "edkm_forward": ([P, i32, pp, P, P, P, P, P], i32),
+            "edkm_reconstruct": ([P, i32, pp, P, P, P, i32, i32, P, P], i32),
+            "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P], i32),
+            "edkm_backward_apply": ([P, i32, pp, P, i32, P, P, P, P, P, i32, P, P], i32),
+            "edkm_backward": ([P, i32, pp, P, i32, P, P, P, P, i32, P, P], i32),
+            "edkm_read_status": ([P, i32, pp, P, P, P], i32),
+            "edkm_last_launch_count": ([], i32),
+            "edkm_status_string": ([i32], ctypes.c_char_p),
+            "edkm_last_error": ([], ctypes.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list:
+    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_forward", "edkm_reconstruct",
+            "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_read_status",
+            "edkm_last_launch_count", "edkm_status_string", "edkm_last_error"]
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise EDKMError(f"{what}: {L.edkm_status_string(rc).decode()} -- {L.edkm_last_error().decode()}")
+
+
+def last_launch_count() -> int:
+    return lib().edkm_last_launch_count()
+
+
+@dataclass(frozen=True)
+class Params:
+    """DKM hyper-parameters (P:31 LUT of k = 2^bits centroids; tau, iterations per DESIGN R3/R4)."""
+    wdtype: torch.dtype = torch.bfloat16
+    bits: int = 3
+    tau: float = 1e-3
+    max_iter: int = 5
+    eps: float = 0.0
+
+    @property
+    def k(self) -> int:
+        return 1 << self.bits
+
+    def c(self) -> _Params:
+        if self.wdtype not in (torch.bfloat16, torch.float16):
+            raise EDKMError("weights must be bfloat16 or float16")
+        return _Params(_DT[self.wdtype], self.bits, float(self.tau), int(self.max_iter), float(self.eps))
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _flat(t: torch.Tensor) -> torch.Tensor:
+    if not t.is_cuda:
+        raise EDKMError("tensors must be CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise EDKMError("tensors must be contiguous")
+    return t.reshape(-1)
+
+
+def _tensor_array(ws):
+    arr = (_Tensor * max(len(ws), 1))()
+    for i, w in enumerate(ws):
+        arr[i].w = w.data_ptr() if w.numel() else None
+        arr[i].n = w.numel()
+    return arr
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * max(len(ts), 1))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr() if t.numel() else None
+    return arr
+
+
+def saved_bytes(nt: int, p: Params) -> int:
+    return lib().edkm_saved_bytes(nt, ctypes.byref(p.c()))
+
+
+def workspace_bytes(nt: int, p: Params) -> int:
+    return lib().edkm_workspace_bytes(nt, ctypes.byref(p.c()))
+
+
+# ----------------------------------------------------------------------------- functional API
+def uniquify(weights, p: Params, counts: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    ws = [_flat(w) for w in weights]
+    for w in ws:
+        if w.dtype != p.wdtype:
+            raise EDKMError("all weights must have the params' dtype")
+    if counts is None:
+        counts = torch.empty((len(ws), PATTERNS), dtype=torch.int32, device=ws[0].device if ws else "cuda")
+    _check(lib().edkm_uniquify(_tensor_array(ws), len(ws), _DT[p.wdtype], _ptr(counts), _stream(stream)),
+           "edkm_uniquify")
+    return counts
+
+
+def forward(counts: torch.Tensor, C0: torch.Tensor, p: Params, saved=None, C_out=None, table=None, stream=None):
+    nt = counts.shape[0]
+    dev = counts.device
+    C0 = C0.to(device=dev, dtype=torch.float32).contiguous()
+    if C0.shape != (nt, p.k):
+        raise EDKMError(f"C0 must have shape ({nt}, {p.k})")
+    if saved is None:
+        saved = torch.empty(saved_bytes(nt, p), dtype=torch.uint8, device=dev)
+    C_out = torch.empty((nt, p.k), dtype=torch.float32, device=dev) if C_out is None else C_out
+    table = torch.empty((nt, PATTERNS), dtype=torch.float32, device=dev) if table is None else table
+    _check(lib().edkm_forward(_ptr(counts), nt, ctypes.byref(p.c()), _ptr(C0), _ptr(C_out), _ptr(table),
+                              _ptr(saved), _stream(stream)), "edkm_forward")
+    return C_out, table, saved
+
+
+def reconstruct(weights, p: Params, table, C_out, saved, mode: int = SOFT, out_dtype: torch.dtype | None = None,
+                outs=None, stream=None):
+    ws = [_flat(w) for w in weights]
+    if out_dtype is None:
+        out_dtype = torch.uint8 if mode == HARD_INDEX else p.wdtype
+    if outs is None:
+        outs = [torch.empty_like(w, dtype=out_dtype) for w in ws]
+    _check(lib().edkm_reconstruct(_tensor_array(ws), len(ws), ctypes.byref(p.c()), _ptr(table), _ptr(C_out),
+                                  _ptr(saved), mode, _DT[out_dtype], _ptr_array([o.reshape(-1) for o in outs]),
+                                  _stream(stream)), "edkm_reconstruct")
+    return outs
+
+
+def backward_reduce(weights, grads, p: Params, counts, saved, ws_buf, gamma=None, stream=None):
+    ws = [_flat(w) for w in weights]
+    gs = [_flat(g) for g in grads]
+    gdt = _DT[gs[0].dtype] if gs else _DT[p.wdtype]
+    gamma = torch.empty((len(ws), p.k), dtype=torch.float64, device=counts.device) if gamma is None else gamma
+    _check(lib().edkm_backward_reduce(_tensor_array(ws), len(ws), ctypes.byref(p.c()), _ptr_array(gs), gdt,
+                                      _ptr(counts), _ptr(saved), _ptr(ws_buf), _ptr(gamma), _stream(stream)),
+           "edkm_backward_reduce")
+    return gamma
+
+
+def backward_apply(weights, grads, p: Params, counts, saved, ws_buf, gamma, dW=None, dw_dtype=None, dC0=None,
+                   stream=None):
+    ws = [_flat(w) for w in weights]
+    gs = [_flat(g) for g in grads]
+    gdt = _DT[gs[0].dtype] if gs else _DT[p.wdtype]
+    dw_dtype = dw_dtype or p.wdtype
+    dW = [torch.empty_like(w, dtype=dw_dtype) for w in ws] if dW is None else dW
+    dC0 = torch.empty((len(ws), p.k), dtype=torch.float32, device=counts.device) if dC0 is None else dC0
+    _check(lib().edkm_backward_apply(_tensor_array(ws), len(ws), ctypes.byref(p.c()), _ptr_array(gs), gdt,
+                                     _ptr(counts), _ptr(saved), _ptr(ws_buf), _ptr(gamma),
+                                     _ptr_array([d.reshape(-1) for d in dW]), _DT[dw_dtype], _ptr(dC0),
+                                     _stream(stream)), "edkm_backward_apply")
+    return dW, dC0
+
+
+def backward(weights, grads, p: Params, counts, saved, ws_buf=None, dW=None, dw_dtype=None, dC0=None, stream=None):
+    ws = [_flat(w) for w in weights]
+    gs = [_flat(g) for g in grads]
+    gdt = _DT[gs[0].dtype] if gs else _DT[p.wdtype]
+    dw_dtype = dw_dtype or p.wdtype
+    if ws_buf is None:
+        ws_buf = torch.empty(workspace_bytes(len(ws), p), dtype=torch.uint8, device=counts.device)
+    dW = [torch.empty_like(w, dtype=dw_dtype) for w in ws] if dW is None else dW
+    dC0 = torch.empty((len(ws), p.k), dtype=torch.float32, device=counts.device) if dC0 is None else dC0
+    _check(lib().edkm_backward(_tensor_array(ws), len(ws), ctypes.byref(p.c()), _ptr_array(gs), gdt, _ptr(counts),
+                               _ptr(saved), _ptr(ws_buf), _ptr_array([d.reshape(-1) for d in dW]), _DT[dw_dtype],
+                               _ptr(dC0), _stream(stream)), "edkm_backward")
+    return dW, dC0
+
+
+def read_status(saved, nt: int, p: Params, stream=None):
+    """(nonfinite weights per tensor, iterations run per tensor); synchronises the stream."""
+    nf = (ctypes.c_int64 * max(nt, 1))()
+    it = (ctypes.c_int32 * max(nt, 1))()
+    _check(lib().edkm_read_status(_ptr(saved), nt, ctypes.byref(p.c()), nf, it, _stream(stream)), "edkm_read_status")
+    return list(nf)[:nt], list(it)[:nt]
+
+
+# ----------------------------------------------------------------------------- reusable step plan
+class Plan:
+    """Buffers of one eDKM step over a fixed list of tensors (no allocation per step).
+
+    A step is: uniquify -> [all-reduce counts] -> forward -> reconstruct ->
+    backward_reduce -> [all-reduce gamma] -> backward_apply.  The bracketed
+    collectives are the caller's (paper_2309_00964_b200.dist); single-process
+    callers skip them.
+    """
+
+    def __init__(self, numels, p: Params, device="cuda"):
+        self.p = p
+        self.nt = len(numels)
+        self.numels = list(numels)
+        dev = torch.device(device)
+        self.counts = torch.empty((self.nt, PATTERNS), dtype=torch.int32, device=dev)
+        self.C_out = torch.empty((self.nt, p.k), dtype=torch.float32, device=dev)
+        self.table = torch.empty((self.nt, PATTERNS), dtype=torch.float32, device=dev)
+        self.saved = torch.empty(saved_bytes(self.nt, p), dtype=torch.uint8, device=dev)
+        self.ws = torch.empty(workspace_bytes(self.nt, p), dtype=torch.uint8, device=dev)
+        self.gamma = torch.empty((self.nt, p.k), dtype=torch.float64, device=dev)
+        self.dC0 = torch.empty((self.nt, p.k), dtype=torch.float32, device=dev)
+        self._cache = {}
+
+    def _arr(self, key, tensors, maker):
+        ptrs = tuple(t.data_ptr() for t in tensors)
+        hit = self._cache.get(key)
+        if hit is None or hit[0] != ptrs:
+            hit = (ptrs, maker([_flat(t) for t in tensors]))
+            self._cache[key] = hit
+        return hit[1]
+
+    def uniquify(self, weights, stream=None):
+        _check(lib().edkm_uniquify(self._arr("w", weights, _tensor_array), self.nt, _DT[self.p.wdtype],
+                                   _ptr(self.counts), _stream(stream)), "edkm_uniquify")
+        return self.counts
+
+    def forward(self, C0, stream=None):
+        _check(lib().edkm_forward(_ptr(self.counts), self.nt, ctypes.byref(self.p.c()), _ptr(C0), _ptr(self.C_out),
+                                  _ptr(self.table), _ptr(self.saved), _stream(stream)), "edkm_forward")
+        return self.C_out
+
+    def reconstruct(self, weights, outs, mode=SOFT, stream=None):
+        odt = _DT[outs[0].dtype] if outs else _DT[self.p.wdtype]
+        _check(lib().edkm_reconstruct(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
+                                      _ptr(self.table), _ptr(self.C_out), _ptr(self.saved), mode, odt,
+                                      self._arr(("o", mode), outs, _ptr_array), _stream(stream)), "edkm_reconstruct")
+        return outs
+
+    def backward_reduce(self, weights, grads, stream=None):
+        gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
+        _check(lib().edkm_backward_reduce(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
+                                          self._arr("g", grads, _ptr_array), gdt, _ptr(self.counts),
+                                          _ptr(self.saved), _ptr(self.ws), _ptr(self.gamma), _stream(stream)),
+               "edkm_backward_reduce")
+        return self.gamma
+
+    def backward_apply(self, weights, grads, dW, stream=None):
+        gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
+        ddt = _DT[dW[0].dtype] if dW else _DT[self.p.wdtype]
+        _check(lib().edkm_backward_apply(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
+                                         self._arr("g", grads, _ptr_array), gdt, _ptr(self.counts), _ptr(self.saved),
+                                         _ptr(self.ws), _ptr(self.gamma), self._arr("dw", dW, _ptr_array), ddt,
+                                         _ptr(self.dC0), _stream(stream)), "edkm_backward_apply")
+        return self.dC0
+
+    def step(self, weights, grads, C0, outs, dW, allreduce=None, stream=None):
+        """One full fwd+bwd over all tensors.  `allreduce(tensor)` sums in place over ranks."""
+        self.uniquify(weights, stream)
+        if allreduce is not None:
+            allreduce(self.counts)
+        self.forward(C0, stream)
+        self.reconstruct(weights, outs, SOFT, stream)
+        self.backward_reduce(weights, grads, stream)
+        if allreduce is not None:
+            allreduce(self.gamma)
+        self.backward_apply(weights, grads, dW, stream)
+        return self.dC0
+
+
+# ----------------------------------------------------------------------------- autograd wrapper
+class EDKMFunction(torch.autograd.Function):
+    """W~ = DKM(W, C0) for one weight tensor on this device (differentiable in W and C0).
+
+    The attention table never materialises per weight: forward saves only the
+    O(T k) trajectory and the per-pattern tables, backward runs TB + B2.
+    """
+
+    @staticmethod
+    def forward(ctx, W, C0, p: Params):
+        w = W.detach().contiguous()
+        counts = uniquify([w], p)
+        C_out, table, saved = forward(counts, C0.detach().reshape(1, -1), p)
+        (Wt,) = reconstruct([w], p, table, C_out, saved, SOFT, W.dtype)
+        ctx.p = p
+        ctx.save_for_backward(w, counts, saved)
+        return Wt.view_as(W)
+
+    @staticmethod
+    def backward(ctx, G):
+        w, counts, saved = ctx.saved_tensors
+        g = G.contiguous()
+        if g.dtype not in (ctx.p.wdtype, torch.float32):
+            g = g.float()
+        (dW,), dC0 = backward([w], [g], ctx.p, counts, saved, dw_dtype=w.dtype)
+        return dW.view_as(w), dC0.reshape(-1), None
+
+
+def edkm(W: torch.Tensor, C0: torch.Tensor, bits: int = 3, tau: float = 1e-3, max_iter: int = 5, eps: float = 0.0):
+    """Differentiable soft-clustered weight W~ (Fig. 1) computed by the CUDA path."""
+    return EDKMFunction.apply(W, C0, Params(W.dtype, bits, tau, max_iter, eps))

@@ -1,0 +1,80 @@
+"""CPU-side checks of the C ABI boundary: libedkm.so builds, loads without a GPU,
+exports every entry point include/edkm.h declares, and rejects bad arguments
+before launching anything (include/edkm.h "Conventions")."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2309_00964_b200 import build as B
+from paper_2309_00964_b200 import edkm as E
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    return E.lib()
+
+
+def declared_functions():
+    h = open(os.path.join(ROOT, "include", "edkm.h")).read()
+    h = re.sub(r"/\*.*?\*/", "", h, flags=re.S)
+    return sorted(set(re.findall(r"\b(edkm_[a-z_]+)\s*\(", h)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("edkm_uniquify", "edkm_forward", "edkm_backward", "edkm_reconstruct"):
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(L):
+    for n in declared_functions():
+        assert hasattr(L, n), n
+    assert sorted(E.exported_symbols()) == declared_functions()
+
+
+def test_bad_arguments_return_errors_without_launch(L):
+    p = E.Params()
+    cp = ctypes.byref(p.c())
+    assert L.edkm_uniquify(None, -1, 0, None, None) == 1
+    assert L.edkm_uniquify(None, 1, 0, None, None) == 1           # NULL tensors
+    assert L.edkm_uniquify(None, 0, 7, None, None) == 2           # bad dtype
+    t = (E._Tensor * 1)()
+    t[0].w, t[0].n = None, 5
+    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None) == 1   # n > 0 with NULL data
+    t[0].w, t[0].n = 3, 5
+    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None) == 1   # odd address
+    for bad in (E._Params(0, 3, -1.0, 5, 0.0), E._Params(0, 3, float("nan"), 5, 0.0), E._Params(0, 3, 1.0, -1, 0.0),
+                E._Params(0, 3, 1.0, 5, -1.0), E._Params(0, 3, float("inf"), 5, 0.0)):
+        assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(bad), ctypes.c_void_p(16), ctypes.c_void_p(16),
+                              ctypes.c_void_p(16), ctypes.c_void_p(16), None) == 1
+    assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(0, 5, 1.0, 5, 0.0)), None, None, None, None,
+                          None) == 4                              # bits > 4: unsupported in this build
+    assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(2, 3, 1.0, 5, 0.0)), None, None, None, None,
+                          None) == 2                              # fp32 weights
+    assert L.edkm_forward(None, 1, cp, None, None, None, None, None) == 1
+    assert L.edkm_saved_bytes(-1, cp) == 0 and L.edkm_saved_bytes(3, cp) > 0
+    assert L.edkm_workspace_bytes(226, cp) >= 226 * 65536 * 24
+    assert L.edkm_last_error()
+    assert L.edkm_status_string(0) == b"EDKM_OK"
+
+
+def test_empty_calls_are_noops(L):
+    p = E.Params()
+    cp = ctypes.byref(p.c())
+    assert L.edkm_uniquify(None, 0, 0, None, None) == 0
+    assert L.edkm_forward(None, 0, cp, None, None, None, None, None) == 0
+    assert L.edkm_backward(None, 0, cp, None, 0, None, None, None, None, 0, None, None) == 0
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2309_00964_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|edkm_oracle|oracle_dkm)", src), f

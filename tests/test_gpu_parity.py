@@ -1,0 +1,291 @@
+"""CUDA path (libedkm.so through the C ABI) vs the CPU oracle, element by element.
+
+Bars:
+  * counts, hard indices, hard values: bit-exact;
+  * C_T, W~ (fp32 output), dW (fp32 output), dC_0: normwise
+    ||x - x_ref||_inf <= 1e-5 ||x_ref||_inf per tensor (north star tolerance);
+  * 16-bit outputs: within 1 ulp of round-to-nearest-even of the oracle value
+    (double rounding / fp64 reordering can flip a tie, R8), plus 1e-5 ||ref|| for dW.
+The oracle runs dense over all |W| x |C| entries (CFG1 sizes) or, at full
+BASELINE sizes, in its pinned attention-table form from exact CPU counts.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2309_00964_b200 import synth
+from paper_2309_00964_b200 import edkm as E
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def bits_of(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16).ravel()
+
+
+def odt(dtype):
+    return O.BF16 if dtype == torch.bfloat16 else O.FP16
+
+
+def normwise(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)) if b.size else 0.0
+
+
+def ulp16(x: np.ndarray, dtype) -> np.ndarray:
+    t = torch.from_numpy(np.abs(x)).to(dtype).to(torch.float64).numpy()
+    mant = 7 if dtype == torch.bfloat16 else 10
+    tiny = 2.0 ** (-133 if dtype == torch.bfloat16 else -24)
+    e = np.floor(np.log2(np.maximum(t, 1e-300)))
+    return np.maximum(2.0 ** (e - mant), tiny)
+
+
+def as16_values(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().to(torch.float64).numpy().ravel()
+
+
+def run_gpu(Ws, Gs, C0, p: E.Params, out_f32=True):
+    """One full step through the C ABI.  Returns dict of numpy results."""
+    dev = torch.device("cuda")
+    Wd = [w.to(dev).reshape(-1) for w in Ws]
+    Gd = [g.to(dev).reshape(-1) for g in Gs]
+    plan = E.Plan([w.numel() for w in Wd], p, dev)
+    C0d = torch.tensor(np.asarray(C0), dtype=torch.float32, device=dev)
+    plan.uniquify(Wd)
+    plan.forward(C0d)
+    odtype = torch.float32 if out_f32 else p.wdtype
+    Wt = [torch.empty(w.numel(), dtype=odtype, device=dev) for w in Wd]
+    plan.reconstruct(Wd, Wt, E.SOFT)
+    Wt16 = [torch.empty(w.numel(), dtype=p.wdtype, device=dev) for w in Wd]
+    plan.reconstruct(Wd, Wt16, E.SOFT)
+    idx = [torch.empty(w.numel(), dtype=torch.uint8, device=dev) for w in Wd]
+    plan.reconstruct(Wd, idx, E.HARD_INDEX)
+    hv = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wd]
+    plan.reconstruct(Wd, hv, E.HARD_VALUE)
+    hv16 = [torch.empty(w.numel(), dtype=p.wdtype, device=dev) for w in Wd]
+    plan.reconstruct(Wd, hv16, E.HARD_VALUE)
+    plan.backward_reduce(Wd, Gd)
+    dW = [torch.empty(w.numel(), dtype=odtype, device=dev) for w in Wd]
+    plan.backward_apply(Wd, Gd, dW)
+    dW16 = [torch.empty(w.numel(), dtype=p.wdtype, device=dev) for w in Wd]
+    plan.backward_apply(Wd, Gd, dW16)
+    torch.cuda.synchronize()
+    nonfin, iters = E.read_status(plan.saved, plan.nt, p)
+    return dict(counts=plan.counts.cpu().numpy(), C=plan.C_out.cpu().numpy(), table=plan.table.cpu().numpy(),
+                Wt=[x.cpu().double().numpy() for x in Wt], Wt16=[as16_values(x) for x in Wt16],
+                idx=[x.cpu().numpy() for x in idx], hv=[x.cpu().numpy() for x in hv],
+                hv16=[bits_of(x) for x in hv16], dW=[x.cpu().double().numpy() for x in dW],
+                dW16=[as16_values(x) for x in dW16], dC0=plan.dC0.cpu().numpy(), gamma=plan.gamma.cpu().numpy(),
+                nonfinite=nonfin, iters=iters)
+
+
+def oracle_dense(w_bits, G, C0, p: E.Params):
+    C0 = np.asarray(C0, np.float32).astype(np.float64)  # the C ABI takes fp32 centroids: same input
+    w = O.decode16(w_bits, odt(p.wdtype))
+    Ct, St, T = O.dkm_forward(w, C0, p.tau, p.max_iter, p.eps)
+    Wt = O.reconstruct(w, Ct[-1], p.tau)
+    dW, dC = O.dkm_backward(w, G, Ct, St, p.tau)
+    return dict(w=w, Ct=Ct, St=St, T=T, Wt=Wt, dW=dW, dC=dC)
+
+
+def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
+    w = ref["w"]
+    fin = np.isfinite(w)
+    # counts: bit-exact (F1)
+    assert np.array_equal(gpu["counts"][t], O.histogram(w_bits).astype(np.int32))
+    assert gpu["iters"][t] == ref["T"]
+    assert gpu["nonfinite"][t] == int((~fin).sum())
+    CT = ref["Ct"][-1]
+    assert normwise(gpu["C"][t], CT) <= TOL, ("C", normwise(gpu["C"][t], CT))
+    # table for every populated finite pattern
+    u = np.nonzero(gpu["counts"][t])[0]
+    uf = u[np.isfinite(O.decode16(u.astype(np.uint16), odt(p.wdtype)))]
+    tab_ref = O.reconstruct(O.decode16(uf.astype(np.uint16), odt(p.wdtype)), CT, p.tau)
+    assert normwise(gpu["table"][t][uf], tab_ref) <= TOL
+    if not dense:
+        return
+    Wt_ref, dW_ref = ref["Wt"], ref["dW"]
+    assert np.all(np.isnan(gpu["Wt"][t][~fin])) and np.all(np.isnan(gpu["dW"][t][~fin]))
+    assert normwise(gpu["Wt"][t][fin], Wt_ref[fin]) <= TOL, ("Wt", normwise(gpu["Wt"][t][fin], Wt_ref[fin]))
+    assert normwise(gpu["dW"][t][fin], dW_ref[fin]) <= TOL, ("dW", normwise(gpu["dW"][t][fin], dW_ref[fin]))
+    # dC0 is returned in fp32: allow its underflow floor for degenerate tensors (n = 1, 2)
+    assert np.max(np.abs(gpu["dC0"][t] - ref["dC"])) <= TOL * np.max(np.abs(ref["dC"])) + 1e-37, \
+        ("dC", gpu["dC0"][t], ref["dC"])
+    # 16-bit outputs: <= 1 ulp of the fp64 oracle value
+    assert np.all(np.abs(gpu["Wt16"][t][fin] - Wt_ref[fin]) <= ulp16(Wt_ref[fin], p.wdtype))
+    lim = ulp16(dW_ref[fin], p.wdtype) + TOL * np.max(np.abs(dW_ref[fin]))
+    assert np.all(np.abs(gpu["dW16"][t][fin] - dW_ref[fin]) <= lim)
+    # hard assignment against the GPU's own fp32 lookup table (R9): bit-exact
+    C32 = gpu["C"][t].astype(np.float32)
+    idx_ref = O.hard_assign(w, C32)
+    idx_ref[~fin] = 0
+    assert np.array_equal(gpu["idx"][t].astype(np.int32), idx_ref)
+    hv_ref = C32[idx_ref]
+    assert np.array_equal(gpu["hv"][t][fin].view(np.uint32), hv_ref[fin].view(np.uint32))
+    hv16_ref = bits_of(torch.from_numpy(hv_ref).to(p.wdtype))
+    assert np.array_equal(gpu["hv16"][t][fin], hv16_ref[fin])
+
+
+# --------------------------------------------------------------------------- CFG1 in full (BASELINE configs[0])
+def test_cfg1_full_parity():
+    wl = synth.workload("cfg1")
+    W = synth.weights(wl, 0)
+    G = synth.grads(wl, 0)
+    C0 = synth.quantile_centroids(wl.k, wl.sigma)
+    p = E.Params(wl.wdtype, wl.bits, wl.tau, wl.max_iter)
+    gpu = run_gpu([W], [G], [C0], p)
+    wb = bits_of(W)
+    ref = oracle_dense(wb, G.double().numpy(), C0, p)
+    assert np.min(ref["St"]) >= 1e-6 * W.numel()
+    check_tensor(gpu, 0, wb, G.double().numpy(), ref, p)
+
+
+# --------------------------------------------------------------------------- sweeps at oracle-friendly sizes
+@pytest.mark.parametrize("dtype,bits,tau,T,sigma,n", [
+    (torch.bfloat16, 3, 1e-4, 5, 0.02, 300_001),
+    (torch.bfloat16, 3, 1e-5, 5, 0.02, 250_000),
+    (torch.bfloat16, 3, 1e-6, 5, 0.02, 200_003),
+    (torch.bfloat16, 1, 1e-3, 3, 1.0, 100_000),
+    (torch.bfloat16, 2, 1e-2, 0, 1.0, 100_000),
+    (torch.bfloat16, 4, 3e-3, 7, 1.0, 150_000),
+    (torch.float16, 4, 1e-5, 30, 0.02, 200_000),
+    (torch.float16, 2, 1e-5, 30, 0.02, 120_007),
+    (torch.float16, 3, 1e-3, 5, 1.0, 131_075),
+])
+def test_parity_sweep(dtype, bits, tau, T, sigma, n):
+    k = 1 << bits
+    W = synth.normal_tensor(n, sigma, dtype, 77 + bits)
+    G = synth.normal_tensor(n, 1e-3, dtype, 99 + bits)
+    C0 = synth.quantile_centroids(k, sigma)
+    p = E.Params(dtype, bits, tau, T)
+    gpu = run_gpu([W], [G], [C0], p)
+    wb = bits_of(W)
+    ref = oracle_dense(wb, G.double().numpy(), C0, p)
+    if T > 0:
+        assert np.min(ref["St"]) >= 1e-6 * n
+    check_tensor(gpu, 0, wb, G.double().numpy(), ref, p)
+
+
+def test_fp32_gradients():
+    n = 100_000
+    W = synth.normal_tensor(n, 0.02, torch.bfloat16, 5)
+    G = synth.normal_tensor(n, 1e-3, torch.float32, 6)
+    C0 = synth.quantile_centroids(8, 0.02)
+    p = E.Params(torch.bfloat16, 3, 1e-5, 5)
+    gpu = run_gpu([W], [G], [C0], p)
+    wb = bits_of(W)
+    check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
+
+
+def test_many_ragged_tensors_and_empty():
+    sizes = [0, 1, 17, 4097, 65536 * 3 + 5, 0, 250_001, 2, 31, 33]
+    p = E.Params(torch.bfloat16, 3, 1e-3, 4)
+    Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 300 + i) for i, n in enumerate(sizes)]
+    Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 400 + i) for i, n in enumerate(sizes)]
+    C0s = [synth.quantile_centroids(8, 1.0) for _ in sizes]
+    gpu = run_gpu(Ws, Gs, C0s, p)
+    for t, n in enumerate(sizes):
+        wb = bits_of(Ws[t])
+        if n == 0:
+            assert gpu["counts"][t].sum() == 0
+            assert np.allclose(gpu["C"][t], C0s[t], rtol=1e-7)  # no data: centroids unchanged (R6)
+            continue
+        ref = oracle_dense(wb, Gs[t].double().numpy(), C0s[t], p)
+        check_tensor(gpu, t, wb, Gs[t].double().numpy(), ref, p)
+
+
+def test_misaligned_slices():
+    base = synth.normal_tensor(200_000, 1.0, torch.bfloat16, 11)
+    gbase = synth.normal_tensor(200_000, 1e-3, torch.bfloat16, 12)
+    p = E.Params(torch.bfloat16, 2, 1e-2, 3)
+    for off in (1, 3, 5, 8, 15):
+        W = base[off:off + 150_001]
+        G = gbase[off:off + 150_001]
+        C0 = synth.quantile_centroids(4, 1.0)
+        gpu = run_gpu([W], [G], [C0], p)
+        wb = bits_of(W)
+        check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
+    # gradient misaligned relative to the weights: scalar path
+    W = base[:150_000]
+    G = gbase[3:150_003]
+    C0 = synth.quantile_centroids(4, 1.0)
+    gpu = run_gpu([W], [G], [C0], p)
+    wb = bits_of(W)
+    check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
+
+
+# --------------------------------------------------------------------------- histogram edge cases (bit-exact)
+@pytest.mark.parametrize("case", ["constant", "every_pattern", "random_bits", "signed_zero", "tiny", "big"])
+def test_uniquify_edge_cases(case):
+    if case == "constant":
+        b = np.full(300_000, 0x3F80, np.uint16)                     # one bin > 65535 (32-way collisions)
+    elif case == "every_pattern":
+        b = np.random.default_rng(0).permutation(65536).astype(np.uint16)
+    elif case == "random_bits":
+        b = np.random.default_rng(1).integers(0, 65536, 1_000_003).astype(np.uint16)  # incl. >= 0xE000 (L2 path)
+    elif case == "signed_zero":
+        b = np.array([0x0000, 0x8000] * 50_001, np.uint16)
+    elif case == "tiny":
+        b = np.array([0xBA45, 0xCB1F, 0xBA45], np.uint16)            # Fig. 3
+    else:
+        b = np.random.default_rng(2).integers(0x3000, 0x3100, (1 << 22) + 3).astype(np.uint16)
+    W = torch.from_numpy(b.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    counts = E.uniquify([W], E.Params(torch.bfloat16))
+    torch.cuda.synchronize()
+    assert np.array_equal(counts.cpu().numpy()[0], O.histogram(b).astype(np.int32))
+
+
+def test_nonfinite_patterns_flagged_and_excluded():
+    n = 100_000
+    W = synth.normal_tensor(n, 1.0, torch.bfloat16, 21)
+    bad = torch.tensor([5, 77, 1000, 99_999])
+    W[bad] = torch.tensor([float("nan"), float("inf"), -float("inf"), float("nan")], dtype=torch.bfloat16)
+    G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 22)
+    C0 = synth.quantile_centroids(8, 1.0)
+    p = E.Params(torch.bfloat16, 3, 1e-3, 5)
+    gpu = run_gpu([W], [G], [C0], p)
+    wb = bits_of(W)
+    ref = oracle_dense(wb, G.double().numpy(), C0, p)
+    check_tensor(gpu, 0, wb, G.double().numpy(), ref, p)
+    assert gpu["nonfinite"][0] == 4
+
+
+def test_eps_mode_iteration_count():
+    # eps stop is "parity unpinned" (R4): check the GPU stops where the oracle does when no near-tie
+    n = 200_000
+    W = synth.normal_tensor(n, 1.0, torch.bfloat16, 31)
+    G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 32)
+    C0 = synth.quantile_centroids(8, 1.0)
+    wb = bits_of(W)
+    w = O.decode16(wb, O.BF16)
+    full, _, _ = O.dkm_forward(w, C0, 1e-3, 60)
+    d = np.max(np.abs(np.diff(full, axis=0)), axis=1)
+    eps = float(np.sqrt(d[10] * d[11]))          # between two iterations, far from either delta
+    assert min(abs(d - eps)) > 1e-9 * np.max(np.abs(full))
+    p = E.Params(torch.bfloat16, 3, 1e-3, 60, eps)
+    gpu = run_gpu([W], [G], [C0], p)
+    ref = oracle_dense(wb, G.double().numpy(), C0, p)
+    check_tensor(gpu, 0, wb, G.double().numpy(), ref, p)
+
+
+def test_autograd_function_matches_oracle():
+    n = 65_537
+    W = synth.normal_tensor(n, 1.0, torch.bfloat16, 41).cuda().requires_grad_()
+    C0 = torch.tensor(synth.quantile_centroids(4, 1.0), device="cuda", requires_grad=True)
+    Wt = E.edkm(W, C0, bits=2, tau=1e-2, max_iter=3)
+    G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 42).cuda()
+    Wt.backward(G)
+    ref = oracle_dense(bits_of(W), G.double().cpu().numpy(), C0.detach().cpu().numpy(), E.Params(torch.bfloat16, 2, 1e-2, 3))
+    assert np.all(np.abs(as16_values(Wt) - ref["Wt"]) <= ulp16(ref["Wt"], torch.bfloat16))
+    assert normwise(C0.grad.cpu().numpy(), ref["dC"]) <= TOL
+    dw = as16_values(W.grad)
+    assert np.all(np.abs(dw - ref["dW"]) <= ulp16(ref["dW"], torch.bfloat16) + TOL * np.max(np.abs(ref["dW"])))
+
+
+def test_launch_counts_are_native():
+    W = synth.normal_tensor(10_000, 1.0, torch.bfloat16, 51).cuda()
+    p = E.Params(torch.bfloat16, 3, 1e-3, 2)
+    E.uniquify([W], p)
+    assert E.last_launch_count() == 1
