@@ -109,10 +109,13 @@ __device__ __forceinline__ int find_tensor(const StreamArgs& A, int64_t e) {
 }
 
 // ---------------------------------------------------------------- magnitude-page window
-// page_cnt[256] (int64, per signed page u>>8, finite populated patterns only) is
+// page_cnt[256] (int64, weights per signed page u>>8, every present pattern) is
 // written by the forward table kernel.  Choose np <= cap consecutive magnitude
-// pages [pbase, pbase+np) that hold the most weights.  Called by one warp.
-__device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, int* out_base, int* out_np) {
+// pages [pbase, pbase+np) that hold the most weights; *out_covers = 1 when the
+// window holds every present pattern (the per-weight kernels then take their
+// fast path with no per-element range check).  Called by one warp.
+__device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, int* out_base, int* out_np,
+                                              int* out_covers) {
   const int lane = threadIdx.x & 31;
   // masses of magnitude pages lane, lane+32, lane+64, lane+96
   int64_t m[4];
@@ -128,8 +131,11 @@ __device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, 
     pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
     pmax = max(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
   }
-  if (pmax < 0) { *out_base = 0; *out_np = 0; return; }
-  if (pmax - pmin + 1 <= cap) { *out_base = pmin; *out_np = pmax - pmin + 1; return; }
+  if (pmax < 0) { if (lane == 0) { *out_base = 0; *out_np = 1; *out_covers = 0; } return; }  // keep np >= 1
+  if (pmax - pmin + 1 <= cap) {
+    if (lane == 0) { *out_base = pmin; *out_np = pmax - pmin + 1; *out_covers = 1; }
+    return;
+  }
   // sliding window of `cap` pages maximising the mass (lane 0, 128 steps)
   __shared__ int64_t s_mass[kMagPages];
 #pragma unroll
@@ -146,6 +152,7 @@ __device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, 
     }
     *out_base = bb;
     *out_np = cap;
+    *out_covers = 0;
   }
   __syncwarp();
 }
@@ -161,4 +168,99 @@ __device__ __forceinline__ uint32_t slot_pattern(int slot, int pbase, int np) {
   return (sign << 15) | ((rel + (uint32_t)pbase) << 8) | ((uint32_t)slot & 0xFFu);
 }
 
+}  // namespace edkm
+
+namespace edkm {
+// ---------------------------------------------------------------- shared-memory primitives (32-bit addresses)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 r;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(a));
+  return r;
+}
+
+// Fast-path window addressing: the window holds every present pattern, so the
+// shared address of pattern u is offP/offN + (u & 0x7FFF) * ES with no range
+// check.  The clamp keeps a caller who breaks the contract (weights differing
+// from those counted) inside the table: wrong values, never a stray write.
+template <int ES>
+struct FastWin {
+  uint32_t offP, offN, lo, hi;
+  __device__ void init(uint32_t base, int pbase, int np) {
+    offP = base - (uint32_t)pbase * 256u * ES;
+    offN = offP + (uint32_t)np * 256u * ES;
+    lo = base;
+    hi = base + (uint32_t)(2 * np * 256 - 1) * ES;
+  }
+  __device__ __forceinline__ uint32_t addr(uint32_t u) const {  // u: 16-bit pattern in the low half
+    const uint32_t a = ((u & 0x8000u) ? offN : offP) + (u & 0x7FFFu) * ES;
+    return min(max(a, lo), hi);
+  }
+};
+}  // namespace edkm
+
+namespace edkm {
+// ---------------------------------------------------------------- windowed per-pattern lookups (predicated, no branch)
+// Window of np magnitude pages from pbase: pattern u is in it iff
+// rel = (u & 0x7FFF) - pbase*256 < np*256 (unsigned); its slot is rel in the
+// positive half (u < 0x8000) or np*256 + rel in the negative half.
+struct Win {
+  uint32_t pb256, np256, baseP, baseN;  // baseP/baseN: shared byte address of slot 0 of each half
+  template <int ES>
+  __device__ void init(uint32_t base, int pbase, int np) {
+    pb256 = (uint32_t)pbase << 8;
+    np256 = (uint32_t)np << 8;
+    baseP = base;
+    baseN = base + np256 * ES;
+  }
+  __device__ __forceinline__ uint32_t rel(uint32_t u) const { return (u & 0x7FFFu) - pb256; }
+  template <int ES>
+  __device__ __forceinline__ uint32_t saddr(uint32_t u, uint32_t r) const { return ((u & 0x8000u) ? baseN : baseP) + r * ES; }
+};
+
+// (phi, psi) of a pattern: shared window when `in` != 0, else the global table
+// entry gtab[u] (its address is formed inside the predicated block).
+__device__ __forceinline__ float2 lookup_f2(uint32_t in, uint32_t saddr, const float2* gtab, uint32_t u) {
+  float2 r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .u64 ga;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+      "@p ld.shared.v2.f32 {%0, %1}, [%3];\n\t"
+      "@!p mad.wide.u32 ga, %5, 8, %4;\n\t"
+      "@!p ld.global.nc.v2.f32 {%0, %1}, [ga];\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(in), "r"(saddr), "l"(gtab), "r"(u));
+  return r;
+}
+
+// Exact 64-bit fixed-point bucket add: when `in` != 0, lo[slot] += q with the
+// carry/borrow into hi[slot] (at saddr + HI_OFF) done by the lane that made it;
+// otherwise the fp64 global bucket gB[u] gets g.  Predicated, no branch.
+template <uint32_t HI_OFF>
+__device__ __forceinline__ void bucket_add(uint32_t in, uint32_t saddr, int q, double* gB, uint32_t u, float g) {
+  asm volatile(
+      "{\n\t.reg .pred p, c, n, f;\n\t.reg .u32 old, nw, d;\n\t.reg .f64 gd;\n\t.reg .u64 ga;\n\t"
+      "setp.ne.u32 p, %0, 0;\n\t"
+      "mov.u32 old, 0;\n\t"
+      "@p atom.shared.add.u32 old, [%1], %2;\n\t"
+      "add.u32 nw, old, %2;\n\t"
+      "setp.lt.u32 c, nw, old;\n\t"
+      "setp.lt.s32 n, %2, 0;\n\t"
+      "xor.pred f, c, n;\n\t"
+      "and.pred f, f, p;\n\t"
+      "selp.u32 d, 1, 0xFFFFFFFF, c;\n\t"
+      "@f red.shared.add.u32 [%1+%6], d;\n\t"
+      "@!p cvt.f64.f32 gd, %3;\n\t"
+      "@!p mad.wide.u32 ga, %5, 8, %4;\n\t"
+      "@!p red.global.add.f64 [ga], gd;\n\t}"
+      ::"r"(in), "r"(saddr), "r"(q), "f"(g), "l"(gB), "r"(u), "n"(HI_OFF)
+      : "memory");
+}
 }  // namespace edkm

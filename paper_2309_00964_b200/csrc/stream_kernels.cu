@@ -45,17 +45,37 @@ __device__ __forceinline__ void for_each_segment(const StreamArgs& A, P& p) {
     if (nv > 0 && !p.vec_ok(t, va)) { head = b - a; nv = 0; }
     for (int64_t i = a + tid; i < a + head; i += bs) p.scalar(t, i);
     int64_t v = tid;
-    for (; v + bs < nv; v += 2 * bs) {
-      typename P::Vec r0, r1;
-      p.load(t, va + 16 * v, r0);
-      p.load(t, va + 16 * (v + bs), r1);
-      p.process(t, va + 16 * v, r0);
-      p.process(t, va + 16 * (v + bs), r1);
-    }
-    if (v < nv) {
-      typename P::Vec r0;
-      p.load(t, va + 16 * v, r0);
-      p.process(t, va + 16 * v, r0);
+    if (P::kLoop == 0) {
+      // one vector per iteration: lowest register use, 1024 threads keep enough loads in flight
+#pragma unroll 1
+      for (; v < nv; v += bs) {
+        typename P::Vec r0;
+        p.load(t, va + 16 * v, r0);
+        p.process(t, va + 16 * v, r0);
+      }
+    } else if (P::kLoop == 2) {
+      // software pipeline: the next vector's loads are in flight while this one is processed
+      typename P::Vec cur, nxt;
+      if (v < nv) p.load(t, va + 16 * v, cur);
+      for (; v < nv; v += bs) {
+        const bool more = v + bs < nv;
+        if (more) p.load(t, va + 16 * (v + bs), nxt);
+        p.process(t, va + 16 * v, cur);
+        if (more) cur = nxt;
+      }
+    } else {
+      for (; v + bs < nv; v += 2 * bs) {
+        typename P::Vec r0, r1;
+        p.load(t, va + 16 * v, r0);
+        p.load(t, va + 16 * (v + bs), r1);
+        p.process(t, va + 16 * v, r0);
+        p.process(t, va + 16 * (v + bs), r1);
+      }
+      if (v < nv) {
+        typename P::Vec r0;
+        p.load(t, va + 16 * v, r0);
+        p.process(t, va + 16 * v, r0);
+      }
     }
     for (int64_t i = va + 16 * nv + tid; i < b; i += bs) p.scalar(t, i);
     p.end(t);
@@ -68,6 +88,7 @@ __device__ __forceinline__ uint32_t pat(const V8& v, int e) { return (v.x[e >> 1
 
 // ============================================================================ F1
 struct F1Policy {
+  static constexpr int kLoop = 1;  // two vectors per iteration
   const StreamArgs& A;
   uint32_t* h;
   int32_t* counts;  // [nt_total][65536], this launch's tensors start at t0
@@ -112,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
 
 template <int MODE>
 struct F2Policy {
+  static constexpr int kLoop = 1;
   const StreamArgs& A;
   const F2Args& F;
   unsigned char* sm;
@@ -131,8 +153,8 @@ struct F2Policy {
       for (int u = threadIdx.x; u < kPatterns; u += blockDim.x)
         tab[u] = pattern_finite(u, A.wdtype) ? round16f(__ldg(C + ix[u]), A.wdtype) : nan16(A.wdtype);
     } else if (MODE == 2) {
-      __shared__ int s_w[2];
-      if (threadIdx.x < 32) choose_window(F.page_cnt + (int64_t)T * 256, kF2Pages32, &s_w[0], &s_w[1]);
+      __shared__ int s_w[3];
+      if (threadIdx.x < 32) choose_window(F.page_cnt + (int64_t)T * 256, kF2Pages32, &s_w[0], &s_w[1], &s_w[2]);
       __syncthreads();
       pbase = s_w[0];
       np = s_w[1];
@@ -214,32 +236,38 @@ __global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_con
 // 64-bit fixed point (lo: u32, hi: i32) with native shared-memory integer
 // atomics -- sm_100 has no native shared fp32 atomic add (it is a CAS loop).
 // The per-segment scale 2^s maps the largest |G| of a 16K-element sample to
-// [2^27, 2^28); an element whose |q| would reach 2^31, or any non-finite G,
-// goes straight to the fp64 global bucket (correct, slower).  The exact
-// per-CTA sum is converted to fp64 once and added to the global bucket.
-
-
-template <int GF32>
+// [2^27, 2^28); a pattern outside the shared window, an element whose |q|
+// would reach 2^31, or a non-finite G goes to the fp64 global bucket instead
+// (predicated, correct, slower).  At the end of the segment the exact per-CTA
+// sums are converted to fp64 once and added to the global buckets.
+// GDT: gradient dtype (kBF16, kFP16, kFP32).
+template <int GDT>
 struct B1Policy {
+  static constexpr int kLoop = 0;
+  static constexpr int GF32 = GDT == kFP32;
+  static constexpr uint32_t kHiOff = 2 * kB1Pages * 256 * 4;  // byte offset of hi[] from lo[]
   const StreamArgs& A;
   const B1Args& Bq;
   uint32_t* lo;
   int32_t* hi;
   int pbase, np;
-  float scale;  // 2^s
+  bool active;   // scale established (some finite nonzero G, representable scale)
+  float scale;   // 2^s
+  uint32_t glim; // bits of (2^31 - 128) / 2^s: |G| below it converts without overflow
   double inv_scale;
-  bool active;  // scale established (some finite nonzero G)
+  Win win;
   struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
   __device__ double* bucket(int t) const { return Bq.B + (int64_t)(A.t0 + t) * kPatterns; }
   __device__ float gval(int t, int64_t i) const {
     if (GF32) return reinterpret_cast<const float*>(A.g[t])[i];
-    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], A.gdtype);
+    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], GDT);
   }
   __device__ void begin(int t, int64_t a, int64_t b) {
-    __shared__ int s_w[2];
+    __shared__ int s_w[3];
     __shared__ unsigned s_max;
     if (threadIdx.x == 0) s_max = 0;
-    if (threadIdx.x < 32) choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB1Pages, &s_w[0], &s_w[1]);
+    if (threadIdx.x < 32)
+      choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB1Pages, &s_w[0], &s_w[1], &s_w[2]);
     __syncthreads();
     pbase = s_w[0];
     np = s_w[1];
@@ -264,16 +292,21 @@ struct B1Policy {
     }
     const unsigned mx = s_max;
     active = false;
+    scale = 0.0f;
+    inv_scale = 0.0;
+    glim = 0;
     if (mx != 0) {
       int e;
       frexpf(__uint_as_float(mx), &e);  // mx in [2^(e-1), 2^e)
       const int s = 28 - e;              // mx * 2^s in [2^27, 2^28)
       if (s <= 126 && s >= -126) {
         active = true;
-        scale = ldexpf(1.0f, s);
-        inv_scale = ldexp(1.0, -s);
+        scale = __int_as_float((127 + s) << 23);
+        inv_scale = __longlong_as_double((long long)(1023 - s) << 52);
+        glim = __float_as_uint(2147483520.0f * (float)inv_scale);  // exact: power-of-two scaling
       }
     }
+    win.init<4>(smem_addr(lo), pbase, np);
     __syncthreads();
   }
   __device__ bool vec_ok(int t, int64_t i) const {
@@ -289,7 +322,8 @@ struct B1Policy {
       r.g[0] = ldg_stream8(reinterpret_cast<const uint16_t*>(A.g[t]) + i);
     }
   }
-  __device__ __forceinline__ void add(int t, uint32_t u, float g) {
+  // generic element (scalar head/tail, segments without a scale)
+  __device__ __forceinline__ void add_slow(int t, uint32_t u, float g) {
     const float x = g * scale;
     const int slot = window_slot(u, pbase, np);
     if (active && slot >= 0 && fabsf(x) < 2147483520.0f) {
@@ -302,16 +336,37 @@ struct B1Policy {
       atomicAdd(&bucket(t)[u], (double)g);
     }
   }
-  __device__ void process(int t, int64_t, const Vec& r) {
+  __device__ __forceinline__ float g_of(const Vec& r, int e) const {
+    if (GF32) return __uint_as_float(r.g[e >> 3].x[e & 7]);
+    if (GDT == kBF16) return __uint_as_float((e & 1) ? (r.g[0].x[e >> 1] & 0xFFFF0000u) : (r.g[0].x[e >> 1] << 16));
+    return decode16f(pat(r.g[0], e), kFP16);
+  }
+  __device__ void process(int t, int64_t i, const Vec& r) {
+    // one range check per 16 elements: every pattern in the window and every |q| < 2^31
+    uint32_t rel[16];
+    uint32_t rmax = 0, gmax = 0;  // gmax: largest |G| bit pattern (NaN > Inf > finite)
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      float g;
-      if (GF32) g = __uint_as_float(r.g[e >> 3].x[e & 7]);
-      else g = decode16f(pat(r.g[0], e), A.gdtype);
-      add(t, pat(r.w, e), g);
+      rel[e] = win.rel(pat(r.w, e));
+      rmax = max(rmax, rel[e]);
+      gmax = max(gmax, __float_as_uint(g_of(r, e)) & 0x7FFFFFFFu);
+    }
+    if (active && rmax < win.np256 && gmax < glim) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t a = win.saddr<4>(pat(r.w, e), rel[e]);
+        const int q = __float2int_rn(g_of(r, e) * scale);
+        const uint32_t old = atom_add_shared(a, (uint32_t)q);
+        const bool carry = old + (uint32_t)q < old;
+        if (carry != (q < 0)) red_add_shared(a + kHiOff, carry ? 1u : 0xFFFFFFFFu);
+      }
+    } else {
+      // rare: re-read the 16 elements (dynamic indexing of the register vector would spill it)
+#pragma unroll 1
+      for (int e = 0; e < 16; ++e) scalar(t, i + e);
     }
   }
-  __device__ void scalar(int t, int64_t i) { add(t, A.w[t][i], gval(t, i)); }
+  __device__ void scalar(int t, int64_t i) { add_slow(t, A.w[t][i], gval(t, i)); }
   __device__ void end(int t) {
     __syncthreads();
     if (active) {
@@ -325,36 +380,42 @@ struct B1Policy {
   }
 };
 
-template <int GF32>
-__global__ void __launch_bounds__(kThreadsB, 1) b1_bucket_kernel(const __grid_constant__ StreamArgs A, const B1Args Bq) {
+template <int GDT>
+__global__ void __launch_bounds__(kThreads, 1) b1_bucket_kernel(const __grid_constant__ StreamArgs A, const B1Args Bq) {
   extern __shared__ __align__(16) uint32_t smem_b1[];
-  B1Policy<GF32> p{A, Bq, smem_b1, reinterpret_cast<int32_t*>(smem_b1 + 2 * kB1Pages * 256), 0, 0, 0.f, 0.0, false};
+  B1Policy<GDT> p{A, Bq, smem_b1, reinterpret_cast<int32_t*>(smem_b1 + 2 * kB1Pages * 256)};
   for_each_segment(A, p);
 }
 
 // ============================================================================ B2
-
-
-template <int GF32, int OF32>
+// dW_i = G_i phi[u_i] + psi[u_i]; (phi, psi) of the window's patterns in shared
+// memory, the rest read from the global table (predicated).
+// GDT: gradient dtype, ODT: dW dtype (kBF16, kFP16, kFP32).
+template <int GDT, int ODT>
 struct B2Policy {
+  static constexpr int kLoop = 0;
+  static constexpr int GF32 = GDT == kFP32, OF32 = ODT == kFP32;
   const StreamArgs& A;
   const B2Args& Bq;
   float2* tab;
   int pbase, np;
+  Win win;
   struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
   __device__ const float2* glob(int t) const { return Bq.phipsi + (int64_t)(A.t0 + t) * kPatterns; }
   __device__ float gval(int t, int64_t i) const {
     if (GF32) return reinterpret_cast<const float*>(A.g[t])[i];
-    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], A.gdtype);
+    return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], GDT);
   }
   __device__ void begin(int t, int64_t, int64_t) {
-    __shared__ int s_w[2];
-    if (threadIdx.x < 32) choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB2Pages, &s_w[0], &s_w[1]);
+    __shared__ int s_w[3];
+    if (threadIdx.x < 32)
+      choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB2Pages, &s_w[0], &s_w[1], &s_w[2]);
     __syncthreads();
     pbase = s_w[0];
     np = s_w[1];
     const float2* src = glob(t);
     for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
+    win.init<8>(smem_addr(tab), pbase, np);
     __syncthreads();
   }
   __device__ bool vec_ok(int t, int64_t i) const {
@@ -371,47 +432,76 @@ struct B2Policy {
       r.g[0] = ldg_stream8(reinterpret_cast<const uint16_t*>(A.g[t]) + i);
     }
   }
-  __device__ __forceinline__ float dw(int t, uint32_t u, float g) const {
+  __device__ __forceinline__ float g_of(const Vec& r, int e) const {
+    if (GF32) return __uint_as_float(r.g[e >> 3].x[e & 7]);
+    if (GDT == kBF16) return __uint_as_float((e & 1) ? (r.g[0].x[e >> 1] & 0xFFFF0000u) : (r.g[0].x[e >> 1] << 16));
+    return decode16f(pat(r.g[0], e), kFP16);
+  }
+  __device__ __forceinline__ float dw_slow(int t, uint32_t u, float g) const {
     const int s = window_slot(u, pbase, np);
     const float2 pp = s >= 0 ? tab[s] : __ldg(glob(t) + u);
     return fmaf(g, pp.x, pp.y);
   }
+  __device__ __forceinline__ uint32_t pack2(float a, float b) const {
+    if (ODT == kBF16) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+      return *reinterpret_cast<const uint32_t*>(&h);
+    }
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
   __device__ void process(int t, int64_t i, const Vec& r) {
-    float d[16];
+    // shared lookups issued speculatively with a clamped slot; one range check per
+    // 16 elements redoes the (rare) out-of-window vector through the generic path
+    const uint32_t lim = win.np256 - 1u;
+    uint32_t rmax = 0;
+    V8 o0, o1;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      float g;
-      if (GF32) g = __uint_as_float(r.g[e >> 3].x[e & 7]);
-      else g = decode16f(pat(r.g[0], e), A.gdtype);
-      d[e] = dw(t, pat(r.w, e), g);
+    for (int q = 0; q < 8; ++q) {
+      float d2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 2 * q + h;
+        const uint32_t u = pat(r.w, e);
+        const uint32_t rr = win.rel(u);
+        rmax = max(rmax, rr);
+        const float2 pp = lds_f2(win.saddr<8>(u, min(rr, lim)));
+        d2[h] = fmaf(g_of(r, e), pp.x, pp.y);
+      }
+      if (OF32) {
+        V8& o = q < 4 ? o0 : o1;
+        o.x[(2 * q) & 7] = __float_as_uint(d2[0]);
+        o.x[(2 * q + 1) & 7] = __float_as_uint(d2[1]);
+      } else {
+        o0.x[q] = pack2(d2[0], d2[1]);
+      }
+    }
+    if (rmax > lim) {
+      // rare: redo the 16 elements from memory (dynamic indexing of the register vector would spill it)
+#pragma unroll 1
+      for (int e = 0; e < 16; ++e) scalar(t, i + e);
+      return;
     }
     if (OF32) {
-      V8 o0, o1;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) { o0.x[e] = __float_as_uint(d[e]); o1.x[e] = __float_as_uint(d[8 + e]); }
       float* out = reinterpret_cast<float*>(A.out[t]) + i;
       stg_stream8(out, o0);
       stg_stream8(out + 8, o1);
     } else {
-      V8 o;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        o.x[q] = (uint32_t)round16f(d[2 * q], A.wdtype) | ((uint32_t)round16f(d[2 * q + 1], A.wdtype) << 16);
-      stg_stream8(reinterpret_cast<uint16_t*>(A.out[t]) + i, o);
+      stg_stream8(reinterpret_cast<uint16_t*>(A.out[t]) + i, o0);
     }
   }
   __device__ void scalar(int t, int64_t i) {
-    const float d = dw(t, A.w[t][i], gval(t, i));
+    const float d = dw_slow(t, A.w[t][i], gval(t, i));
     if (OF32) reinterpret_cast<float*>(A.out[t])[i] = d;
-    else reinterpret_cast<uint16_t*>(A.out[t])[i] = round16f(d, A.wdtype);
+    else reinterpret_cast<uint16_t*>(A.out[t])[i] = round16f(d, ODT);
   }
   __device__ void end(int) { __syncthreads(); }
 };
 
-template <int GF32, int OF32>
-__global__ void __launch_bounds__(kThreadsB, 1) b2_dw_kernel(const __grid_constant__ StreamArgs A, const B2Args Bq) {
+template <int GDT, int ODT>
+__global__ void __launch_bounds__(kThreads, 1) b2_dw_kernel(const __grid_constant__ StreamArgs A, const B2Args Bq) {
   extern __shared__ __align__(16) float2 smem_b2[];
-  B2Policy<GF32, OF32> p{A, Bq, smem_b2, 0, 0};
+  B2Policy<GDT, ODT> p{A, Bq, smem_b2};
   for_each_segment(A, p);
 }
 
@@ -459,33 +549,49 @@ cudaError_t launch_f2(const StreamArgs& A, const F2Args& F, int mode, int sms, c
   return cudaGetLastError();
 }
 
+template <int GDT>
+static cudaError_t launch_b1_t(const StreamArgs& A, const B1Args& Bq, int sms, cudaStream_t s) {
+  const size_t smem = 2 * kB1Pages * 256 * 8;
+  cudaError_t e = set_smem((const void*)b1_bucket_kernel<GDT>, smem);
+  if (e != cudaSuccess) return e;
+  b1_bucket_kernel<GDT><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, Bq);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_b1(const StreamArgs& A, const B1Args& Bq, int sms, cudaStream_t s) {
   if (A.total == 0) return cudaSuccess;
-  const size_t smem = 2 * kB1Pages * 256 * 8;
-  const bool f32 = A.gdtype == kFP32;
-  const void* fn = f32 ? (const void*)b1_bucket_kernel<1> : (const void*)b1_bucket_kernel<0>;
-  cudaError_t e = set_smem(fn, smem);
+  switch (A.gdtype) {
+    case kBF16: return launch_b1_t<kBF16>(A, Bq, sms, s);
+    case kFP16: return launch_b1_t<kFP16>(A, Bq, sms, s);
+    default: return launch_b1_t<kFP32>(A, Bq, sms, s);
+  }
+}
+
+template <int GDT, int ODT>
+static cudaError_t launch_b2_t(const StreamArgs& A, const B2Args& Bq, int sms, cudaStream_t s) {
+  const size_t smem = 2 * kB2Pages * 256 * 8;
+  cudaError_t e = set_smem((const void*)b2_dw_kernel<GDT, ODT>, smem);
   if (e != cudaSuccess) return e;
-  const int g = grid_for(A.total, sms);
-  if (f32) b1_bucket_kernel<1><<<g, kThreadsB, smem, s>>>(A, Bq);
-  else b1_bucket_kernel<0><<<g, kThreadsB, smem, s>>>(A, Bq);
+  b2_dw_kernel<GDT, ODT><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, Bq);
   return cudaGetLastError();
+}
+
+template <int GDT>
+static cudaError_t launch_b2_g(const StreamArgs& A, const B2Args& Bq, int sms, cudaStream_t s) {
+  switch (A.odtype) {
+    case kBF16: return launch_b2_t<GDT, kBF16>(A, Bq, sms, s);
+    case kFP16: return launch_b2_t<GDT, kFP16>(A, Bq, sms, s);
+    default: return launch_b2_t<GDT, kFP32>(A, Bq, sms, s);
+  }
 }
 
 cudaError_t launch_b2(const StreamArgs& A, const B2Args& Bq, int sms, cudaStream_t s) {
   if (A.total == 0) return cudaSuccess;
-  const size_t smem = 2 * kB2Pages * 256 * 8;
-  const int gf = A.gdtype == kFP32, of = A.odtype == kFP32;
-  const void* fn = gf ? (of ? (const void*)b2_dw_kernel<1, 1> : (const void*)b2_dw_kernel<1, 0>)
-                      : (of ? (const void*)b2_dw_kernel<0, 1> : (const void*)b2_dw_kernel<0, 0>);
-  cudaError_t e = set_smem(fn, smem);
-  if (e != cudaSuccess) return e;
-  const int g = grid_for(A.total, sms);
-  if (gf && of) b2_dw_kernel<1, 1><<<g, kThreadsB, smem, s>>>(A, Bq);
-  else if (gf) b2_dw_kernel<1, 0><<<g, kThreadsB, smem, s>>>(A, Bq);
-  else if (of) b2_dw_kernel<0, 1><<<g, kThreadsB, smem, s>>>(A, Bq);
-  else b2_dw_kernel<0, 0><<<g, kThreadsB, smem, s>>>(A, Bq);
-  return cudaGetLastError();
+  switch (A.gdtype) {
+    case kBF16: return launch_b2_g<kBF16>(A, Bq, sms, s);
+    case kFP16: return launch_b2_g<kFP16>(A, Bq, sms, s);
+    default: return launch_b2_g<kFP32>(A, Bq, sms, s);
+  }
 }
 
 }  // namespace edkm

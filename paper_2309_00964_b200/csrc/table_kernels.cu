@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     const bool pop = fin && c > 0;
     if (!fin) nonfin += c;
     const unsigned b = __ballot_sync(0xffffffffu, pop);
-    long long pm = fin ? c : 0;
+    long long pm = c;  // all present patterns (finite or not) pick the per-weight windows
 #pragma unroll
     for (int o = 16; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
     if (lane == 0) { s_scan[warp] = __popc(b); s_pg[warp] = pm; }
