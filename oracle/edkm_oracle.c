@@ -363,10 +363,12 @@ int oracle_dkm_backward(const double* w, const double* G, int64_t n, int k, doub
 /* phi[u], psi[u], dC.  Used only to check the paper's central claim against */
 /* the dense form above (tests) and to reach large sizes quickly.            */
 /* ------------------------------------------------------------------------ */
+/* gammaT_in: if non-NULL, gamma_T is taken from it (e.g. the sum of per-learner partials,
+ * P:79) instead of being accumulated from B, which may then be NULL. */
 int oracle_dkm_backward_table(const double* v, const double* cnt, const double* B, int64_t m, int k, double tau,
-                              int T, const double* C_traj, const double* S_traj, double* phi, double* psi,
-                              double* dC) {
-    if (k < 1 || k > ORACLE_MAX_K || !(tau > 0) || T < 0 || m < 0) return -1;
+                              int T, const double* C_traj, const double* S_traj, const double* gammaT_in,
+                              double* phi, double* psi, double* dC) {
+    if (k < 1 || k > ORACLE_MAX_K || !(tau > 0) || T < 0 || m < 0 || (!B && !gammaT_in)) return -1;
     double A[ORACLE_MAX_K], ghat[ORACLE_MAX_K];
     double gamma[ORACLE_MAX_K] = {0};
     const double* CT = C_traj + (int64_t)T * k;
@@ -376,12 +378,14 @@ int oracle_dkm_backward_table(const double* v, const double* cnt, const double* 
         for (int l = 0; l < k; ++l) Wt += A[l] * CT[l];
         double direct = 0.0;
         for (int l = 0; l < k; ++l) {
-            gamma[l] += B[u] * A[l] * (1.0 + (CT[l] - Wt) * 2.0 * (v[u] - CT[l]) / tau);
+            if (!gammaT_in) gamma[l] += B[u] * A[l] * (1.0 + (CT[l] - Wt) * 2.0 * (v[u] - CT[l]) / tau);
             direct += A[l] * (CT[l] - Wt) * (-2.0 * (v[u] - CT[l]) / tau);
         }
         phi[u] = direct;
         psi[u] = 0.0;
     }
+    if (gammaT_in)
+        for (int l = 0; l < k; ++l) gamma[l] = gammaT_in[l];
     for (int t = T - 1; t >= 0; --t) {
         const double* Ct = C_traj + (int64_t)t * k;
         const double* Cn = C_traj + (int64_t)(t + 1) * k;

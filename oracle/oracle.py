@@ -65,7 +65,7 @@ def _load():
         _lib.oracle_hard_assign.restype = None
         _lib.oracle_dkm_backward.argtypes = [P, P, i64, i32, f64, i32, P, P, i32, P, P]
         _lib.oracle_dkm_backward.restype = i32
-        _lib.oracle_dkm_backward_table.argtypes = [P, P, P, i64, i32, f64, i32, P, P, P, P, P]
+        _lib.oracle_dkm_backward_table.argtypes = [P, P, P, i64, i32, f64, i32, P, P, P, P, P, P]
         _lib.oracle_dkm_backward_table.restype = i32
     return _lib
 
@@ -153,16 +153,21 @@ def dkm_backward(w, G, C_traj, S_traj, tau: float, nthreads: int = 0):
     return dW, dC
 
 
-def dkm_backward_table(v, cnt, B, C_traj, S_traj, tau: float):
+def dkm_backward_table(v, cnt, B, C_traj, S_traj, tau: float, gammaT=None):
     """Attention-table backward on unique values v with counts cnt and bucket sums
-    B[u] = sum_{i in u} G_i.  Returns (phi[m], psi[m], dC0[k]); dW_i = G_i phi + psi."""
-    v, cnt, B = _f64(v).ravel(), _f64(cnt).ravel(), _f64(B).ravel()
+    B[u] = sum_{i in u} G_i.  Returns (phi[m], psi[m], dC0[k]); dW_i = G_i phi + psi.
+    If gammaT is given (e.g. summed over learners) it replaces sum_u B[u] f_T(u, .)
+    and B may be None.  With T = 0 the returned dC0 is gamma_T itself."""
+    v, cnt = _f64(v).ravel(), _f64(cnt).ravel()
+    B = None if B is None else _f64(B).ravel()
+    g = None if gammaT is None else _f64(gammaT).ravel()
     Ct, St = _f64(C_traj), _f64(S_traj)
     T, k = Ct.shape[0] - 1, Ct.shape[1]
     St = St if St.size else np.zeros((1, k))
     phi, psi, dC = np.empty(v.size), np.empty(v.size), np.empty(k)
-    rc = _load().oracle_dkm_backward_table(_p(v), _p(cnt), _p(B), v.size, k, float(tau), T, _p(Ct),
-                                           _p(np.ascontiguousarray(St)), _p(phi), _p(psi), _p(dC))
+    rc = _load().oracle_dkm_backward_table(_p(v), _p(cnt), None if B is None else _p(B), v.size, k, float(tau), T,
+                                           _p(Ct), _p(np.ascontiguousarray(St)), None if g is None else _p(g),
+                                           _p(phi), _p(psi), _p(dC))
     if rc != 0:
         raise ValueError("oracle_dkm_backward_table: bad arguments")
     return phi, psi, dC

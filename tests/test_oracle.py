@@ -307,6 +307,15 @@ def test_attention_table_form_equals_dense_map(k, tau, T):
     phi, psi, dCu = O.dkm_backward_table(v, cnt, B, Ct, St, tau)
     assert normwise(G * phi[inv] + psi[inv], dW) < 1e-11
     assert normwise(dCu, dC) < 1e-11
+    # gamma_T is linear in B: sharding the weights into two halves and summing the
+    # per-half gamma_T (T = 0 call returns gamma_T) reproduces the unsharded backward
+    half = n // 2
+    g_parts = []
+    for sl in (slice(0, half), slice(half, n)):
+        Bp = np.bincount(inv[sl], weights=G[sl], minlength=u.size)
+        g_parts.append(O.dkm_backward_table(v, cnt, Bp, Ct[-1:], St[:0], tau)[2])
+    phi2, psi2, dC2 = O.dkm_backward_table(v, cnt, None, Ct, St, tau, gammaT=g_parts[0] + g_parts[1])
+    assert normwise(dC2, dC) < 1e-11 and normwise(G * phi2[inv] + psi2[inv], dW) < 1e-11
     # phi is the direct path: G-independent and non-negative, phi = (2/tau) Var_A(C)
     A = O.attention(v, Ct[-1], tau)
     var = (A * (Ct[-1][None] - (A @ Ct[-1])[:, None]) ** 2).sum(1)
