@@ -16,7 +16,7 @@
 namespace edkm {
 
 constexpr int kThreads = 1024;   // F1, F2
-constexpr int kThreadsB = 512;   // B1, B2: two inputs per element need more registers
+
 constexpr int kF1Bins = 57344;  // patterns < 0xE000 counted in SMEM (224 KiB); the rest in L2
 constexpr int kB1Pages = 55;    // magnitude pages per sign kept by B1 (8 B/pattern)
 constexpr int kB2Pages = 55;    // B2 (float2 phi, psi)

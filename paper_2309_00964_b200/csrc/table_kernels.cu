@@ -1,4 +1,4 @@
-// table_kernels.cu -- the table phase of the eDKM hot path (S3).
+// table_kernels.cu -- the table phase of the eDKM hot path (S4).
 //
 // The DKM attention map ("O(|W||C|)") is never formed per weight: by
 // uniquification (P:77 S2.2, Fig. 3) every per-weight quantity depends on the
@@ -12,11 +12,12 @@
 //   TB      reverse loop t = T-1..0 giving psi[u], dC_0; phi[u] = (2/tau) Var_{A_T[u]}(C_T).
 //
 // One thread-block cluster per tensor (cl CTAs); rows are split into cl
-// contiguous pattern partitions; k-vector sums are reduced per thread in row
-// order, then by warp shuffles, across warps in warp order and across the
-// cluster through DSMEM in CTA order -- deterministic, identical on every CTA.
-// All arithmetic is fp64 (exp included): DESIGN.md R7 shows fp32 table-phase
-// arithmetic misses the 1e-5 parity bound.  Cost is O(U k T), independent of N.
+// contiguous pattern partitions.  Each CTA stages its rows (value v_u, count
+// n_u, running psi) in shared memory once, so the T-loops touch no global
+// memory; k-vector sums are reduced per thread in row order, then by warp
+// shuffles, across warps in warp order and across the cluster through DSMEM in
+// CTA order -- deterministic and identical on every CTA and every rank.
+// All arithmetic is fp64 (exp included): DESIGN.md R7.  Cost O(U k T), independent of N.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -28,6 +29,8 @@ namespace edkm {
 
 constexpr int kTThreads = 512;
 constexpr int kTWarps = kTThreads / 32;
+constexpr int kStage = 6144;  // rows per CTA staged in shared memory (v, n, psi: 24 B each)
+constexpr size_t kStageBytes = (size_t)kStage * 24;
 
 template <int K>
 __device__ __forceinline__ void attention_row(double v, const double* C, double inv_tau, double (&A)[K]) {
@@ -79,36 +82,99 @@ __device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, d
   __syncthreads();
 }
 
+// Rows of one partition: patterns in rows[], values/counts staged in shared memory
+// for r < kStage, re-derived from global memory beyond (rare: U > kStage per CTA).
+struct RowStage {
+  const uint16_t* rows;
+  const int32_t* cnt;
+  double* sv;    // [kStage] value v_u
+  double* sn;    // [kStage] count n_u
+  double* spsi;  // [kStage] psi accumulator (TB)
+  double* gpsi;  // global psi for r >= kStage
+  int nr, wdtype;
+  __device__ __forceinline__ double v(int r) const { return r < kStage ? sv[r] : decode16(rows[r], wdtype); }
+  __device__ __forceinline__ double n(int r) const { return r < kStage ? sn[r] : (double)cnt[rows[r]]; }
+  __device__ __forceinline__ double& psi(int r) const { return r < kStage ? spsi[r] : gpsi[r]; }
+  __device__ void stage() {
+    for (int r = threadIdx.x; r < nr && r < kStage; r += blockDim.x) {
+      const uint32_t u = rows[r];
+      sv[r] = decode16(u, wdtype);
+      sn[r] = (double)cnt[u];
+    }
+    __syncthreads();
+  }
+};
+
 // ============================================================================ TF
 template <int K>
 __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   __shared__ double sC[K], sCn[K], sCf[K], sDelta[K];
   __shared__ double red[kTWarps * 2 * K], part[2 * 2 * K], tot[2 * K];
   __shared__ int s_scan[kTWarps];
-  __shared__ long long s_pg[kTWarps], s_nf[kTWarps];
+  __shared__ long long s_nf[kTWarps];
 
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
   const int chunk = kPatterns / cl, base = crank * chunk;
   uint16_t* rows = P.rows + (int64_t)t * kPatterns + base;
   TensorState* st = P.state + t;
+  float* tab = P.table + (int64_t)t * kPatterns;
+  uint16_t* tab16 = P.table16 + (int64_t)t * kPatterns;
+  uint8_t* idx = P.idx8 + (int64_t)t * kPatterns;
 
-  // ---- 1. compact populated finite patterns of this partition (ascending u); page masses
+  // ---- 1. compact populated finite patterns of this partition (ascending u), 16 per thread per step;
+  //         page masses (every present pattern), non-finite counts, NaN-fill of the W~ tables
   int nr = 0;
   long long nonfin = 0;
-  for (int off = 0; off < chunk; off += kTThreads) {
-    const uint32_t u = (uint32_t)(base + off + tid);
-    const int c = cnt[u];
-    const bool fin = pattern_finite(u, P.wdtype);
-    const bool pop = fin && c > 0;
-    if (!fin) nonfin += c;
-    const unsigned b = __ballot_sync(0xffffffffu, pop);
-    long long pm = c;  // all present patterns (finite or not) pick the per-weight windows
+  for (int off = 0; off < chunk; off += kTThreads * 16) {
+    const int u0 = base + off + tid * 16;
+    int c[16];
+    const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
-    if (lane == 0) { s_scan[warp] = __popc(b); s_pg[warp] = pm; }
+    for (int q = 0; q < 4; ++q) {
+      const int4 x = __ldg(c4 + q);
+      c[4 * q] = x.x;
+      c[4 * q + 1] = x.y;
+      c[4 * q + 2] = x.z;
+      c[4 * q + 3] = x.w;
+    }
+    unsigned popmask = 0;
+    long long pm = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const bool fin = pattern_finite(u0 + e, P.wdtype);
+      if (fin && c[e] > 0) popmask |= 1u << e;
+      if (!fin) nonfin += c[e];
+      pm += c[e];
+    }
+    // NaN fill (populated entries are overwritten in phase 3); hard index 0 for non-finite patterns
+    const float nanf = __int_as_float(0x7FC00000);
+    float4* t4 = reinterpret_cast<float4*>(tab + u0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t4[q] = make_float4(nanf, nanf, nanf, nanf);
+    const uint32_t n16 = nan16(P.wdtype) * 0x10001u;
+    uint4* h4 = reinterpret_cast<uint4*>(tab16 + u0);
+    h4[0] = make_uint4(n16, n16, n16, n16);
+    h4[1] = make_uint4(n16, n16, n16, n16);
+    if (!pattern_finite(u0, P.wdtype) || !pattern_finite(u0 + 15, P.wdtype))
+      for (int e = 0; e < 16; ++e)
+        if (!pattern_finite(u0 + e, P.wdtype)) idx[u0 + e] = 0;
+    // one signed page = 256 patterns = 16 threads
+#pragma unroll
+    for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
+    if ((lane & 15) == 0) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
+    // block exclusive scan of the per-thread populated counts
+    const int np = __popc(popmask);
+    int incl = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_scan[warp] = incl;
     __syncthreads();
     int woff = 0, btot = 0;
     for (int w = 0; w < kTWarps; ++w) {
@@ -116,11 +182,11 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
       woff += (w < warp) ? x : 0;
       btot += x;
     }
-    if (pop) rows[nr + woff + __popc(b & ((1u << lane) - 1u))] = (uint16_t)u;
-    if (tid < kTThreads / 256) {  // one signed page = 256 patterns = 8 warps
-      long long s = 0;
-      for (int w = 0; w < 8; ++w) s += s_pg[tid * 8 + w];
-      P.page_cnt[(int64_t)t * 256 + ((base + off) >> 8) + tid] = s;
+    int pos = nr + woff + incl - np;
+    while (popmask) {
+      const int e = __ffs(popmask) - 1;
+      popmask &= popmask - 1;
+      rows[pos++] = (uint16_t)(u0 + e);
     }
     nr += btot;
     __syncthreads();
@@ -128,7 +194,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) nonfin += __shfl_xor_sync(0xffffffffu, nonfin, o);
   if (lane == 0) s_nf[warp] = nonfin;
-  __syncthreads();
+  __syncthreads();  // also orders the rows[] writes before staging
   if (tid == 0) {
     long long s = 0;
     for (int w = 0; w < kTWarps; ++w) s += s_nf[w];
@@ -136,6 +202,8 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     st->nrows[crank] = nr;
     if (crank == 0) st->cl = cl;
   }
+  RowStage R{rows, cnt, stage_mem, stage_mem + kStage, stage_mem + 2 * kStage, nullptr, nr, P.wdtype};
+  R.stage();
 
   // ---- 2. unrolled centroid updates
   const int stride_c = (P.max_iter + 1) * K, stride_s = (P.max_iter > 0 ? P.max_iter : 1) * K;
@@ -152,8 +220,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
 #pragma unroll
     for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
     for (int r = tid; r < nr; r += kTThreads) {
-      const uint32_t u = rows[r];
-      const double v = decode16(u, P.wdtype), n = (double)cnt[u];
+      const double v = R.v(r), n = R.n(r);
       double A[K];
       attention_row<K>(v, sC, P.inv_tau, A);
 #pragma unroll
@@ -193,35 +260,25 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   }
   __syncthreads();
 
-  // ---- 3. W~ table (populated patterns), 16-bit rounding, hard index (all finite patterns)
-  float* tab = P.table + (int64_t)t * kPatterns;
-  uint16_t* tab16 = P.table16 + (int64_t)t * kPatterns;
-  uint8_t* idx = P.idx8 + (int64_t)t * kPatterns;
-  for (int u = base + tid; u < base + chunk; u += kTThreads) {
-    const bool fin = pattern_finite(u, P.wdtype);
-    const double v = decode16(u, P.wdtype);
+  // ---- 3. per populated pattern: W~ (fp32 and 16-bit), hard index vs the fp32 C_out
+  for (int r = tid; r < nr; r += kTThreads) {
+    const uint32_t u = rows[r];
+    const double v = R.v(r);
     int best = 0;
-    if (fin) {
-      double bd = (v - sCf[0]) * (v - sCf[0]);
+    double bd = (v - sCf[0]) * (v - sCf[0]);
 #pragma unroll
-      for (int j = 1; j < K; ++j) {
-        const double d = (v - sCf[j]) * (v - sCf[j]);
-        if (d < bd) { bd = d; best = j; }
-      }
+    for (int j = 1; j < K; ++j) {
+      const double d = (v - sCf[j]) * (v - sCf[j]);
+      if (d < bd) { bd = d; best = j; }
     }
     idx[u] = (uint8_t)best;
-    if (fin && cnt[u] > 0) {
-      double A[K];
-      attention_row<K>(v, sC, P.inv_tau, A);
-      double wt = 0.0;
+    double A[K];
+    attention_row<K>(v, sC, P.inv_tau, A);
+    double wt = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) wt += A[j] * sC[j];
-      tab[u] = (float)wt;
-      tab16[u] = round16(wt, P.wdtype);
-    } else {
-      tab[u] = __int_as_float(0x7FC00000);
-      tab16[u] = nan16(P.wdtype);
-    }
+    for (int j = 0; j < K; ++j) wt += A[j] * sC[j];
+    tab[u] = (float)wt;
+    tab16[u] = round16(wt, P.wdtype);
   }
   cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
 }
@@ -266,6 +323,7 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
 template <int K>
 __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   __shared__ double sG[K], sCt[K], sCn[K], sInvS[K], red[kTWarps * K], part[2 * K], tot[K];
   const TensorState* st = P.state + t;
@@ -274,6 +332,13 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   const double* ctraj = P.ctraj + (int64_t)t * (P.max_iter + 1) * K;
   const double* straj = P.straj + (int64_t)t * (P.max_iter > 0 ? P.max_iter : 1) * K;
   double* psi = P.psi + (int64_t)t * kPatterns;
+  // this CTA owns partitions p = crank, crank + cl, ...; with pcl == cl (always, same
+  // heuristic in TF) that is the single partition `crank`, staged in shared memory
+  const bool one = pcl == cl;
+  const int chunk = kPatterns / pcl;
+  RowStage R{P.rows + (int64_t)t * kPatterns + crank * chunk, cnt, stage_mem, stage_mem + kStage,
+             stage_mem + 2 * kStage, psi + crank * chunk, one ? st->nrows[crank] : 0, P.wdtype};
+  if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
   for (int it = T - 1; it >= 0; --it) {
@@ -288,12 +353,12 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
 #pragma unroll
     for (int l = 0; l < K; ++l) acc[l] = 0.0;
     for (int p = crank; p < pcl; p += cl) {
-      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * (kPatterns / pcl);
-      double* psi_p = psi + p * (kPatterns / pcl);
-      const int nr = st->nrows[p];
+      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
+      double* gpsi = psi + p * chunk;
+      const int nr = one ? R.nr : st->nrows[p];
       for (int r = tid; r < nr; r += kTThreads) {
-        const uint32_t u = rows[r];
-        const double v = decode16(u, P.wdtype), n = (double)cnt[u];
+        const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
+        const double n = one ? R.n(r) : (double)cnt[rows[r]];
         double A[K], gh[K];
         attention_row<K>(v, sCt, P.inv_tau, A);
         double s = 0.0, dpsi = 0.0;
@@ -310,7 +375,8 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
           dpsi -= rr * dz;
           acc[l] += n * rr * dz;
         }
-        psi_p[r] = (it == T - 1 ? 0.0 : psi_p[r]) + dpsi;
+        double& ps = one ? R.psi(r) : gpsi[r];
+        ps = (it == T - 1 ? 0.0 : ps) + dpsi;
       }
     }
     cluster_allreduce<K>(acc, red, part, tot, it & 1, cluster);
@@ -323,12 +389,12 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   __syncthreads();
   float2* pp = P.phipsi + (int64_t)t * kPatterns;
   for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * (kPatterns / pcl);
-    const double* psi_p = psi + p * (kPatterns / pcl);
-    const int nr = st->nrows[p];
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
+    double* gpsi = psi + p * chunk;
+    const int nr = one ? R.nr : st->nrows[p];
     for (int r = tid; r < nr; r += kTThreads) {
       const uint32_t u = rows[r];
-      const double v = decode16(u, P.wdtype);
+      const double v = one ? R.v(r) : decode16(u, P.wdtype);
       double A[K];
       attention_row<K>(v, sCt, P.inv_tau, A);
       double wt = 0.0;
@@ -337,10 +403,10 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       double var = 0.0;
 #pragma unroll
       for (int l = 0; l < K; ++l) var += A[l] * (sCt[l] - wt) * (sCt[l] - wt);
-      pp[u] = make_float2((float)(2.0 * P.inv_tau * var), T > 0 ? (float)psi_p[r] : 0.0f);
+      const double ps = T > 0 ? (one ? R.psi(r) : gpsi[r]) : 0.0;
+      pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
     }
     // NaN/Inf patterns: dW = NaN (R10)
-    const int chunk = kPatterns / pcl;
     for (int u = p * chunk + tid; u < (p + 1) * chunk; u += kTThreads)
       if (!pattern_finite(u, P.wdtype)) pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
   }
@@ -355,33 +421,41 @@ int table_cluster_size(int nt) {
   return 1;
 }
 
-#define EDKM_TABLE_LAUNCH(NAME, KERNEL)                                                          \
-  cudaError_t NAME(const TableArgs& P, cudaStream_t s) {                                           \
-    if (P.nt == 0) return cudaSuccess;                                                             \
-    void (*fn)(const TableArgs);                                                                   \
-    switch (P.k) {                                                                                 \
-      case 2: fn = KERNEL<2>; break;                                                               \
-      case 4: fn = KERNEL<4>; break;                                                               \
-      case 8: fn = KERNEL<8>; break;                                                               \
-      case 16: fn = KERNEL<16>; break;                                                             \
-      default: return cudaErrorInvalidValue;                                                       \
-    }                                                                                              \
-    cudaLaunchConfig_t cfg = {};                                                                   \
-    cfg.gridDim = dim3((unsigned)(P.nt * P.cl));                                                   \
-    cfg.blockDim = dim3(kTThreads);                                                                \
-    cfg.stream = s;                                                                                \
-    cudaLaunchAttribute attr[1];                                                                   \
-    attr[0].id = cudaLaunchAttributeClusterDimension;                                              \
-    attr[0].val.clusterDim.x = (unsigned)P.cl;                                                     \
-    attr[0].val.clusterDim.y = 1;                                                                  \
-    attr[0].val.clusterDim.z = 1;                                                                  \
-    cfg.attrs = attr;                                                                              \
-    cfg.numAttrs = 1;                                                                              \
-    return cudaLaunchKernelEx(&cfg, fn, P);                                                        \
+template <class Fn>
+static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_t smem) {
+  if (P.nt == 0) return cudaSuccess;
+  if (smem) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.nt * P.cl));
+  cfg.blockDim = dim3(kTThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)P.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, P);
+}
+
+#define EDKM_TABLE_LAUNCH(NAME, KERNEL, SMEM)             \
+  cudaError_t NAME(const TableArgs& P, cudaStream_t s) {    \
+    switch (P.k) {                                          \
+      case 2: return launch_table(P, s, KERNEL<2>, SMEM);   \
+      case 4: return launch_table(P, s, KERNEL<4>, SMEM);   \
+      case 8: return launch_table(P, s, KERNEL<8>, SMEM);   \
+      case 16: return launch_table(P, s, KERNEL<16>, SMEM); \
+      default: return cudaErrorInvalidValue;                \
+    }                                                       \
   }
 
-EDKM_TABLE_LAUNCH(launch_tf, tf_kernel)
-EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel)
-EDKM_TABLE_LAUNCH(launch_tb, tb_kernel)
+EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytes)
+EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0)
+EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytes)
 
 }  // namespace edkm

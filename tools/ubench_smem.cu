@@ -60,7 +60,7 @@ __global__ void k_read(const uint4* w, size_t n16, uint32_t* out) {
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k_hist(const uint4* w, size_t n16, uint32_t* gout) {
   extern __shared__ uint32_t h[];
-  const int nw = (MODE == 3) ? 16384 : 32768;
+  const int nw = (MODE == 3) ? 16384 : (MODE >= 10 ? 57344 : 32768);
   for (int i = threadIdx.x; i < nw; i += blockDim.x) h[i] = 0;
   __syncthreads();
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -84,6 +84,10 @@ __global__ void __launch_bounds__(1024, 1) k_hist(const uint4* w, size_t n16, ui
           uint32_t a = (uint32_t)__cvta_generic_to_shared(&h[u >> 1]);
           if (u & 1u) asm volatile("red.shared.add.u32 [%0], 65536;" :: "r"(a));
           else asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(a));
+        } else if (MODE >= 10) {  // C = MODE-10 copies interleaved: word = idx*C + lane%C, idx in [0, 224K/4/C)
+          constexpr int C = MODE - 10;
+          const uint32_t idx = u % (57344u / C);
+          asm volatile("red.shared.add.u32 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&h[idx * C + (threadIdx.x & (C - 1))])));
         } else if (MODE == 2) {
           asm volatile("red.shared.add.u32 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(&h[u & 0x7FFFu])), "r"(1u));
         } else {
@@ -96,6 +100,32 @@ __global__ void __launch_bounds__(1024, 1) k_hist(const uint4* w, size_t n16, ui
   __syncthreads();
   uint32_t s = spill;
   for (int i = threadIdx.x; i < nw; i += blockDim.x) s += h[i];
+  if (s == 0x12345678u) gout[0] = s;
+}
+
+// L2 atomics: fraction 1/F of elements (u % F == 0) go to red.global on a 256 KB counter array, rest to SMEM
+template <int F>
+__global__ void __launch_bounds__(1024, 1) k_hist_l2(const uint4* w, size_t n16, uint32_t* gcnt, uint32_t* gout) {
+  extern __shared__ uint32_t h[];
+  for (int i = threadIdx.x; i < 57344; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += stride) {
+    uint4 v = ldg_stream(w + i);
+    uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t u = (wd[q] >> (16 * hh)) & 0xFFFFu;
+        if (F == 1 || (u % F) == 0) asm volatile("red.global.add.u32 [%0], 1;" :: "l"(gcnt + u));
+        else asm volatile("red.shared.add.u32 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&h[u % 57344u])));
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t s = 0;
+  for (int i = threadIdx.x; i < 57344; i += blockDim.x) s += h[i];
   if (s == 0x12345678u) gout[0] = s;
 }
 
@@ -147,6 +177,24 @@ int main() {
   run("hist packed u16 atom+ret", [&] { k_hist<0><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("hist packed u16 red", [&] { k_hist<1><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("hist packed 2x const red", [&] { k_hist<4><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
+  for (int m : {11, 12, 14, 18}) {}
+  cudaFuncSetAttribute(k_hist<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist<18>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  run("hist 1 copy  (57344 bins)", [&] { k_hist<11><<<sms, 1024, 229376>>>((const uint4*)w, n16, o); }, n * 2.0);
+  run("hist 2 copies interleaved", [&] { k_hist<12><<<sms, 1024, 229376>>>((const uint4*)w, n16, o); }, n * 2.0);
+  run("hist 4 copies interleaved", [&] { k_hist<14><<<sms, 1024, 229376>>>((const uint4*)w, n16, o); }, n * 2.0);
+  run("hist 8 copies interleaved", [&] { k_hist<18><<<sms, 1024, 229376>>>((const uint4*)w, n16, o); }, n * 2.0);
+  uint32_t* gcnt; CK(cudaMalloc(&gcnt, 65536 * 4 * 4));
+  cudaFuncSetAttribute(k_hist_l2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist_l2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist_l2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  cudaFuncSetAttribute(k_hist_l2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  run("hist all L2 red", [&] { k_hist_l2<1><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
+  run("hist 1/2 L2 red", [&] { k_hist_l2<2><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
+  run("hist 1/4 L2 red", [&] { k_hist_l2<4><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
+  run("hist 1/8 L2 red", [&] { k_hist_l2<8><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
   run("hist u32 32K red", [&] { k_hist<2><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom", [&] { k_hist<3><<<sms, 1024, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom 3x/SM", [&] { k_hist<3><<<sms * 3, 1024 / 2, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
