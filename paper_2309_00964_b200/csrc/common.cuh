@@ -226,6 +226,23 @@ struct Win {
   __device__ __forceinline__ uint32_t saddr(uint32_t u, uint32_t r) const { return ((u & 0x8000u) ? baseN : baseP) + r * ES; }
 };
 
+// Exact 64-bit fixed-point add into the shared bucket at saddr (lo u32) / saddr+HI_OFF (hi i32):
+// lo += q; the lane whose add carried out of (or borrowed from) lo moves +-1 into hi.
+template <uint32_t HI_OFF>
+__device__ __forceinline__ void fixed_add(uint32_t saddr, int q) {
+  asm volatile(
+      "{\n\t.reg .pred c, n, f;\n\t.reg .u32 old, nw, d;\n\t"
+      "atom.shared.add.u32 old, [%0], %1;\n\t"
+      "add.u32 nw, old, %1;\n\t"
+      "setp.lt.u32 c, nw, old;\n\t"
+      "setp.lt.s32 n, %1, 0;\n\t"
+      "xor.pred f, c, n;\n\t"
+      "selp.u32 d, 1, 0xFFFFFFFF, c;\n\t"
+      "@f red.shared.add.u32 [%0+%2], d;\n\t}"
+      ::"r"(saddr), "r"(q), "n"(HI_OFF)
+      : "memory");
+}
+
 // (phi, psi) of a pattern: shared window when `in` != 0, else the global table
 // entry gtab[u] (its address is formed inside the predicated block).
 __device__ __forceinline__ float2 lookup_f2(uint32_t in, uint32_t saddr, const float2* gtab, uint32_t u) {

@@ -253,7 +253,9 @@ struct B1Policy {
   int pbase, np;
   bool active;   // scale established (some finite nonzero G, representable scale)
   float scale;   // 2^s
-  uint32_t glim; // bits of (2^31 - 128) / 2^s: |G| below it converts without overflow
+  uint32_t glim;   // fp32 bits of (2^31 - 128) / 2^s: |G| below it converts without overflow
+  uint32_t glim16; // the same bound for 16-bit G bit patterns (NaN/Inf excluded)
+  uint32_t negpb2; // -pbase*256 in both 16-bit halves
   double inv_scale;
   Win win;
   struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
@@ -295,6 +297,7 @@ struct B1Policy {
     scale = 0.0f;
     inv_scale = 0.0;
     glim = 0;
+    glim16 = 0;
     if (mx != 0) {
       int e;
       frexpf(__uint_as_float(mx), &e);  // mx in [2^(e-1), 2^e)
@@ -304,9 +307,13 @@ struct B1Policy {
         scale = __int_as_float((127 + s) << 23);
         inv_scale = __longlong_as_double((long long)(1023 - s) << 52);
         glim = __float_as_uint(2147483520.0f * (float)inv_scale);  // exact: power-of-two scaling
+        const float lim = __uint_as_float(glim);
+        if (GDT == kBF16) glim16 = min((glim + 0xFFFFu) >> 16, 0x7F80u);
+        else glim16 = lim >= 65504.0f ? 0x7C00u : (uint32_t)__half_as_ushort(__float2half_ru(lim));
       }
     }
     win.init<4>(smem_addr(lo), pbase, np);
+    negpb2 = ((0x10000u - win.pb256) & 0xFFFFu) * 0x10001u;
     __syncthreads();
   }
   __device__ bool vec_ok(int t, int64_t i) const {
@@ -342,23 +349,29 @@ struct B1Policy {
     return decode16f(pat(r.g[0], e), kFP16);
   }
   __device__ void process(int t, int64_t i, const Vec& r) {
-    // one range check per 16 elements: every pattern in the window and every |q| < 2^31
-    uint32_t rel[16];
-    uint32_t rmax = 0, gmax = 0;  // gmax: largest |G| bit pattern (NaN > Inf > finite)
+    // Window offsets of the 16 patterns two at a time (16x2 SIMD): rel = (u & 0x7FFF) - pbase*256
+    // and slot = sign * np*256 + rel; one range check per vector (every rel < np*256 and every
+    // |G| below the overflow limit, NaN/Inf included) selects the fast path.
+    uint32_t slot2[8];
+    uint32_t rmax2 = 0, gmax = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      rel[e] = win.rel(pat(r.w, e));
-      rmax = max(rmax, rel[e]);
-      gmax = max(gmax, __float_as_uint(g_of(r, e)) & 0x7FFFFFFFu);
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t x = r.w.x[q];
+      const uint32_t r2 = __vadd2(x & 0x7FFF7FFFu, negpb2);
+      rmax2 = __vmaxu2(rmax2, r2);
+      slot2[q] = ((x >> 15) & 0x00010001u) * win.np256 + r2;
+      if (GF32) {
+        gmax = max(gmax, max(r.g[q >> 2].x[(2 * q) & 7] & 0x7FFFFFFFu, r.g[q >> 2].x[(2 * q + 1) & 7] & 0x7FFFFFFFu));
+      } else {
+        gmax = __vmaxu2(gmax, r.g[0].x[q] & 0x7FFF7FFFu);
+      }
     }
-    if (active && rmax < win.np256 && gmax < glim) {
+    const bool ok = GF32 ? gmax < glim : (max(gmax & 0xFFFFu, gmax >> 16) < glim16);
+    if (active && max(rmax2 & 0xFFFFu, rmax2 >> 16) < win.np256 && ok) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const uint32_t a = win.saddr<4>(pat(r.w, e), rel[e]);
-        const int q = __float2int_rn(g_of(r, e) * scale);
-        const uint32_t old = atom_add_shared(a, (uint32_t)q);
-        const bool carry = old + (uint32_t)q < old;
-        if (carry != (q < 0)) red_add_shared(a + kHiOff, carry ? 1u : 0xFFFFFFFFu);
+        const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
+        fixed_add<kHiOff>(win.baseP + slot * 4, __float2int_rn(g_of(r, e) * scale));
       }
     } else {
       // rare: re-read the 16 elements (dynamic indexing of the register vector would spill it)
@@ -399,6 +412,7 @@ struct B2Policy {
   const B2Args& Bq;
   float2* tab;
   int pbase, np;
+  uint32_t negpb2;  // -pbase*256 in both 16-bit halves
   Win win;
   struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
   __device__ const float2* glob(int t) const { return Bq.phipsi + (int64_t)(A.t0 + t) * kPatterns; }
@@ -416,6 +430,7 @@ struct B2Policy {
     const float2* src = glob(t);
     for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
     win.init<8>(smem_addr(tab), pbase, np);
+    negpb2 = ((0x10000u - win.pb256) & 0xFFFFu) * 0x10001u;
     __syncthreads();
   }
   __device__ bool vec_ok(int t, int64_t i) const {
@@ -451,21 +466,24 @@ struct B2Policy {
     return *reinterpret_cast<const uint32_t*>(&h);
   }
   __device__ void process(int t, int64_t i, const Vec& r) {
-    // shared lookups issued speculatively with a clamped slot; one range check per
-    // 16 elements redoes the (rare) out-of-window vector through the generic path
+    // shared lookups issued speculatively with a clamped slot (16x2 SIMD offsets, as in B1);
+    // one range check per 16 elements redoes the (rare) out-of-window vector via the generic path
     const uint32_t lim = win.np256 - 1u;
-    uint32_t rmax = 0;
+    const uint32_t lim2 = lim * 0x10001u;
+    uint32_t rmax2 = 0;
     V8 o0, o1;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
+      const uint32_t x = r.w.x[q];
+      const uint32_t r2 = __vadd2(x & 0x7FFF7FFFu, negpb2);
+      rmax2 = __vmaxu2(rmax2, r2);
+      const uint32_t s2 = ((x >> 15) & 0x00010001u) * win.np256 + __vminu2(r2, lim2);
       float d2[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = 2 * q + h;
-        const uint32_t u = pat(r.w, e);
-        const uint32_t rr = win.rel(u);
-        rmax = max(rmax, rr);
-        const float2 pp = lds_f2(win.saddr<8>(u, min(rr, lim)));
+        const uint32_t slot = h ? (s2 >> 16) : (s2 & 0xFFFFu);
+        const float2 pp = lds_f2(win.baseP + slot * 8);
         d2[h] = fmaf(g_of(r, e), pp.x, pp.y);
       }
       if (OF32) {
@@ -476,6 +494,7 @@ struct B2Policy {
         o0.x[q] = pack2(d2[0], d2[1]);
       }
     }
+    const uint32_t rmax = max(rmax2 & 0xFFFFu, rmax2 >> 16);
     if (rmax > lim) {
       // rare: redo the 16 elements from memory (dynamic indexing of the register vector would spill it)
 #pragma unroll 1
