@@ -78,3 +78,11 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|edkm_oracle|oracle_dkm)", src), f
+
+
+def test_pipeline_groups_cover_tensors_in_order():
+    from paper_2309_00964_b200.pipeline import _groups
+    for numels, g in (([5, 1, 1, 1, 10, 3], 3), ([1] * 10, 4), ([100], 8), ([0, 0, 5], 2)):
+        gs = _groups(numels, g)
+        assert sum(gs, []) == list(range(len(numels)))
+        assert 1 <= len(gs) <= g and all(gs)

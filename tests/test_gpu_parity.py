@@ -289,3 +289,28 @@ def test_launch_counts_are_native():
     p = E.Params(torch.bfloat16, 3, 1e-3, 2)
     E.uniquify([W], p)
     assert E.last_launch_count() == 1
+
+
+def test_host_pipeline_matches_oracle():
+    """pipeline.HostPipeline: host-resident W, G through three overlapped streams, per tensor group."""
+    from paper_2309_00964_b200.pipeline import HostPipeline
+    sizes = [50_000, 7, 120_001, 65_536, 3_000, 90_000]
+    p = E.Params(torch.bfloat16, 2, 1e-2, 3)
+    Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 900 + i) for i, n in enumerate(sizes)]
+    Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 950 + i) for i, n in enumerate(sizes)]
+    C0 = torch.tensor([synth.quantile_centroids(4, 1.0)] * len(sizes), dtype=torch.float32, device="cuda")
+    hW = [w.pin_memory() for w in Ws]
+    hG = [g.pin_memory() for g in Gs]
+    hWt = [torch.empty_like(w).pin_memory() for w in Ws]
+    hdW = [torch.empty_like(w).pin_memory() for w in Ws]
+    pipe = HostPipeline(sizes, p, "cuda", n_groups=3)
+    assert len(pipe.groups) == 3 and sorted(sum(pipe.groups, [])) == list(range(len(sizes)))
+    dC = pipe.step(hW, hG, C0, hWt, hdW)
+    torch.cuda.synchronize()
+    dC = torch.cat([d.cpu() for d in dC]).numpy()
+    for t in range(len(sizes)):
+        ref = oracle_dense(bits_of(Ws[t]), Gs[t].double().numpy(), C0[t].cpu().numpy(), p)
+        assert np.all(np.abs(as16_values(hWt[t]) - ref["Wt"]) <= ulp16(ref["Wt"], torch.bfloat16))
+        lim = ulp16(ref["dW"], torch.bfloat16) + TOL * np.max(np.abs(ref["dW"]))
+        assert np.all(np.abs(as16_values(hdW[t]) - ref["dW"]) <= lim)
+        assert np.max(np.abs(dC[t] - ref["dC"])) <= TOL * np.max(np.abs(ref["dC"])) + 1e-37
