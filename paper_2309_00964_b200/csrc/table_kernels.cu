@@ -17,7 +17,8 @@
 // memory; k-vector sums are reduced per thread in row order, then by warp
 // shuffles, across warps in warp order and across the cluster through DSMEM in
 // CTA order -- deterministic and identical on every CTA and every rank.
-// All arithmetic is fp64 (exp included): DESIGN.md R7.  Cost O(U k T), independent of N.
+// Sums, centroids and the backward recursion are fp64; the attention exponentials are fp32
+// on an accurately reduced argument (attention_row, R7).  Cost O(U k T), independent of N.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -32,24 +33,72 @@ constexpr int kTWarps = kTThreads / 32;
 constexpr int kStage = 6144;  // rows per CTA staged in shared memory (v, n, psi: 24 B each)
 constexpr size_t kStageBytes = (size_t)kStage * 24;
 
+// Centroids of one iteration in the forms the attention needs: fp64 values, a float-float
+// split (hi + lo), and per centroid pair (m, j) the fp64-derived difference C_m - C_j
+// (fp32) and sum C_m + C_j (float-float).
 template <int K>
-__device__ __forceinline__ void attention_row(double v, const double* C, double inv_tau, double (&A)[K]) {
-  double d[K];
-  double dmin = d[0] = (v - C[0]) * (v - C[0]);
-#pragma unroll
-  for (int j = 1; j < K; ++j) {
-    d[j] = (v - C[j]) * (v - C[j]);
-    dmin = fmin(dmin, d[j]);
+struct CSet {
+  double c[K];
+  float hi[K], lo[K];
+  float dm[K][K];          // C_m - C_j
+  float ph[K][K], pl[K][K];  // C_m + C_j = ph + pl
+  // every thread of the block calls it; the caller synchronises before and after
+  __device__ void prepare(const double* src) {
+    const int t = threadIdx.x;
+    if (t < K * K) {
+      const double a = src[t / K], b = src[t % K], p = a + b;
+      dm[t / K][t % K] = (float)(a - b);
+      const float h = (float)p;
+      ph[t / K][t % K] = h;
+      pl[t / K][t % K] = (float)(p - (double)h);
+    }
+    if (t < K) {
+      c[t] = src[t];
+      hi[t] = (float)src[t];
+      lo[t] = (float)(src[t] - (double)hi[t]);
+    }
   }
-  double Z = 0.0;
+};
+
+// DKM attention of one pattern value v (exact in fp32: a 16-bit float) to the K centroids:
+//   A_j = exp(-(d_j - d_min)/tau) / sum_l exp(-(d_l - d_min)/tau),  d_j = (v - C_j)^2.
+// With m = argmin_j |v - C_j|, d_j - d_m = (C_m - C_j)(2v - C_m - C_j).  The second factor
+// is 2v - (ph + pl) in fp32: exact where it is small (2v and ph within a factor 2,
+// Sterbenz), so near a cluster boundary -- where A is most sensitive -- the logit carries
+// relative, not absolute, fp32 error (~1e-7).  exp(-x) = 2^-y is split as 2^-f * 2^-n
+// (n = floor y): 2^-f in fp32 (MUFU), 2^-n applied exactly in fp64, so tiny weights keep
+// the range of fp64 exp.  A is returned normalised in fp64; callers sum in fp64 (R7).
+template <int K>
+__device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float sc, double (&A)[K]) {
+  int jm = 0;
+  float am = INFINITY;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    A[j] = exp(-(d[j] - dmin) * inv_tau);
-    Z += A[j];
+    const float a = fabsf((vf - cs.hi[j]) - cs.lo[j]);
+    if (a < am) { am = a; jm = j; }
   }
-  const double iz = 1.0 / Z;
+  const float* dmr = cs.dm[jm];
+  const float* phr = cs.ph[jm];
+  const float* plr = cs.pl[jm];
+  const float v2 = 2.0f * vf;
+  float a[K];
+  int nexp[K];
+  float Z = 0.0f;
 #pragma unroll
-  for (int j = 0; j < K; ++j) A[j] *= iz;
+  for (int j = 0; j < K; ++j) {
+    const float s = (v2 - phr[j]) - plr[j];
+    const float y = (dmr[j] * s) * sc;  // >= ~0: exponent in base 2
+    const float n = floorf(y);
+    nexp[j] = (int)n;
+    a[j] = exp2f(n - y);                               // 2^-f, in (0.5, 1]
+    Z += nexp[j] < 126 ? __int_as_float((127 - nexp[j]) << 23) * a[j] : 0.0f;  // fp32 is enough for Z >= ~1
+  }
+  const float iz = 1.0f / Z;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double p2 = nexp[j] > 1022 ? 0.0 : __longlong_as_double((long long)(1023 - nexp[j]) << 52);  // 2^-n
+    A[j] = (double)(a[j] * iz) * p2;
+  }
 }
 
 // Sum N doubles over the CTA then over the cluster; result in tot[0..N) of every CTA.
@@ -114,6 +163,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   const int lane = tid & 31, warp = tid >> 5;
   __shared__ double sC[K], sCn[K], sCf[K], sDelta[K];
   __shared__ double red[kTWarps * 2 * K], part[2 * 2 * K], tot[2 * K];
+  __shared__ CSet<K> cs;
   __shared__ int s_scan[kTWarps];
   __shared__ long long s_nf[kTWarps];
 
@@ -214,20 +264,22 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     if (crank == 0) ctraj[tid] = sC[tid];
   }
   __syncthreads();
+  const float sc = (float)(P.inv_tau * 1.4426950408889634);  // 1/tau in exp2 units
   int T = P.max_iter;
   for (int it = 0; it < P.max_iter; ++it) {
+    cs.prepare(sC);
+    __syncthreads();
     double acc[2 * K];
 #pragma unroll
     for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
     for (int r = tid; r < nr; r += kTThreads) {
-      const double v = R.v(r), n = R.n(r);
+      const double v = R.v(r), n = R.n(r), nv = n * v;
       double A[K];
-      attention_row<K>(v, sC, P.inv_tau, A);
+      attention_row<K>((float)v, cs, sc, A);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const double na = n * A[j];
-        acc[j] += na;
-        acc[K + j] += na * v;
+        acc[j] = fma(A[j], n, acc[j]);
+        acc[K + j] = fma(A[j], nv, acc[K + j]);
       }
     }
     cluster_allreduce<2 * K>(acc, red, part, tot, it & 1, cluster);
@@ -258,6 +310,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     if (crank == 0) P.C_out[(int64_t)t * K + tid] = cf;
     sCf[tid] = (double)cf;  // the deployable fp32 lookup table (R9)
   }
+  cs.prepare(sC);
   __syncthreads();
 
   // ---- 3. per populated pattern: W~ (fp32 and 16-bit), hard index vs the fp32 C_out
@@ -273,10 +326,10 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     }
     idx[u] = (uint8_t)best;
     double A[K];
-    attention_row<K>(v, sC, P.inv_tau, A);
+    attention_row<K>((float)v, cs, sc, A);
     double wt = 0.0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) wt += A[j] * sC[j];
+    for (int j = 0; j < K; ++j) wt = fma(A[j], cs.c[j], wt);
     tab[u] = (float)wt;
     tab16[u] = round16(wt, P.wdtype);
   }
@@ -288,11 +341,14 @@ template <int K>
 __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double sC[K], red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ double red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ CSet<K> cs;
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
-  if (tid < K) sC[tid] = P.ctraj[(int64_t)t * (P.max_iter + 1) * K + (int64_t)T * K + tid];
+  cs.prepare(P.ctraj + (int64_t)t * (P.max_iter + 1) * K + (int64_t)T * K);
   __syncthreads();
+  const double* sC = cs.c;
+  const float sc = (float)(P.inv_tau * 1.4426950408889634);
   const double* Bt = P.B + (int64_t)t * kPatterns;
   double acc[K];
 #pragma unroll
@@ -305,11 +361,10 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
       const double B = Bt[u];
       if (B == 0.0) continue;
       const double v = decode16(u, P.wdtype);
-      double A[K];
-      attention_row<K>(v, sC, P.inv_tau, A);
-      double wt = 0.0;
+      double A[K], wt = 0.0;
+      attention_row<K>((float)v, cs, sc, A);
 #pragma unroll
-      for (int l = 0; l < K; ++l) wt += A[l] * sC[l];
+      for (int l = 0; l < K; ++l) wt = fma(A[l], sC[l], wt);
 #pragma unroll
       for (int l = 0; l < K; ++l) acc[l] += B * A[l] * (1.0 + (sC[l] - wt) * 2.0 * (v - sC[l]) * P.inv_tau);
     }
@@ -325,7 +380,10 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double sG[K], sCt[K], sCn[K], sInvS[K], red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ double sG[K], sCn[K], sInvS[K], red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ CSet<K> cs;
+  const double* sCt = cs.c;
+  const float sc = (float)(P.inv_tau * 1.4426950408889634);
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
@@ -342,8 +400,8 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
   for (int it = T - 1; it >= 0; --it) {
+    cs.prepare(ctraj + (int64_t)it * K);
     if (tid < K) {
-      sCt[tid] = ctraj[(int64_t)it * K + tid];
       sCn[tid] = ctraj[(int64_t)(it + 1) * K + tid];
       const double S = straj[(int64_t)it * K + tid];
       sInvS[tid] = S != 0.0 ? 1.0 / S : 0.0;
@@ -360,7 +418,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
         const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
         const double n = one ? R.n(r) : (double)cnt[rows[r]];
         double A[K], gh[K];
-        attention_row<K>(v, sCt, P.inv_tau, A);
+        attention_row<K>((float)v, cs, sc, A);
         double s = 0.0, dpsi = 0.0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
@@ -385,7 +443,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   }
   if (crank == 0 && tid < K) P.dC0[(int64_t)t * K + tid] = (float)sG[tid];
   // (phi, psi) table: phi[u] = (2/tau) sum_l A_T[u,l] (C_T[l] - W~_u)^2
-  if (tid < K) sCt[tid] = ctraj[(int64_t)T * K + tid];
+  cs.prepare(ctraj + (int64_t)T * K);
   __syncthreads();
   float2* pp = P.phipsi + (int64_t)t * kPatterns;
   for (int p = crank; p < pcl; p += cl) {
@@ -396,10 +454,10 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       const uint32_t u = rows[r];
       const double v = one ? R.v(r) : decode16(u, P.wdtype);
       double A[K];
-      attention_row<K>(v, sCt, P.inv_tau, A);
+      attention_row<K>((float)v, cs, sc, A);
       double wt = 0.0;
 #pragma unroll
-      for (int l = 0; l < K; ++l) wt += A[l] * sCt[l];
+      for (int l = 0; l < K; ++l) wt = fma(A[l], sCt[l], wt);
       double var = 0.0;
 #pragma unroll
       for (int l = 0; l < K; ++l) var += A[l] * (sCt[l] - wt) * (sCt[l] - wt);

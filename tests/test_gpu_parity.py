@@ -90,6 +90,14 @@ def oracle_dense(w_bits, G, C0, p: E.Params):
     return dict(w=w, Ct=Ct, St=St, T=T, Wt=Wt, dW=dW, dC=dC)
 
 
+def within(got, ref, lim, what):
+    bad = ~(np.abs(got - ref) <= lim)
+    if bad.any():
+        i = np.flatnonzero(bad)[:5]
+        raise AssertionError(f"{what}: {bad.sum()} of {bad.size} outside the bound; e.g. got {got[i]} ref {ref[i]} "
+                             f"lim {np.broadcast_to(lim, ref.shape)[i]}")
+
+
 def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
     w = ref["w"]
     fin = np.isfinite(w)
@@ -98,6 +106,15 @@ def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
     assert gpu["iters"][t] == ref["T"]
     assert gpu["nonfinite"][t] == int((~fin).sum())
     CT = ref["Ct"][-1]
+    if ref["T"] > 0 and np.min(ref["St"]) < 1e-6 * max(int(fin.sum()), 1):
+        # dead cluster (R6): its centroid is set by exp() tails far below any rounding level, so
+        # C_T / W~ / dW / dC_0 are "parity unpinned"; check what is still defined
+        assert np.all(np.isfinite(gpu["C"][t]))
+        C32 = gpu["C"][t].astype(np.float32)
+        idx_ref = O.hard_assign(w, C32)
+        idx_ref[~fin] = 0
+        assert np.array_equal(gpu["idx"][t].astype(np.int32), idx_ref)
+        return
     assert normwise(gpu["C"][t], CT) <= TOL, ("C", normwise(gpu["C"][t], CT))
     # table for every populated finite pattern
     u = np.nonzero(gpu["counts"][t])[0]
@@ -110,13 +127,18 @@ def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
     assert np.all(np.isnan(gpu["Wt"][t][~fin])) and np.all(np.isnan(gpu["dW"][t][~fin]))
     assert normwise(gpu["Wt"][t][fin], Wt_ref[fin]) <= TOL, ("Wt", normwise(gpu["Wt"][t][fin], Wt_ref[fin]))
     assert normwise(gpu["dW"][t][fin], dW_ref[fin]) <= TOL, ("dW", normwise(gpu["dW"][t][fin], dW_ref[fin]))
-    # dC0 is returned in fp32: allow its underflow floor for degenerate tensors (n = 1, 2)
-    assert np.max(np.abs(gpu["dC0"][t] - ref["dC"])) <= TOL * np.max(np.abs(ref["dC"])) + 1e-37, \
+    # dC_0 normwise; its floor is set by the size of the summands (~sum |G|), below which the
+    # fp64 oracle itself only carries cancellation residue (e.g. tiny tensors where every
+    # cluster collapses onto its own weights and dL/dC_0 ~ 1e-26)
+    floor = 1e-9 * float(np.sum(np.abs(G[fin]))) if G is not None else 0.0
+    assert np.max(np.abs(gpu["dC0"][t] - ref["dC"])) <= TOL * max(np.max(np.abs(ref["dC"])), floor) + 1e-37, \
         ("dC", gpu["dC0"][t], ref["dC"])
-    # 16-bit outputs: <= 1 ulp of the fp64 oracle value
-    assert np.all(np.abs(gpu["Wt16"][t][fin] - Wt_ref[fin]) <= ulp16(Wt_ref[fin], p.wdtype))
+    # 16-bit outputs: <= 1 ulp of the fp64 oracle value, plus the normwise 1e-5 allowance where
+    # W~ cancels to ~0 between centroids of opposite sign (R7, R8)
+    within(gpu["Wt16"][t][fin], Wt_ref[fin], ulp16(Wt_ref[fin], p.wdtype) + TOL * np.max(np.abs(Wt_ref[fin])),
+           "W~ 16-bit")
     lim = ulp16(dW_ref[fin], p.wdtype) + TOL * np.max(np.abs(dW_ref[fin]))
-    assert np.all(np.abs(gpu["dW16"][t][fin] - dW_ref[fin]) <= lim)
+    within(gpu["dW16"][t][fin], dW_ref[fin], lim, "dW 16-bit")
     # hard assignment against the GPU's own fp32 lookup table (R9): bit-exact
     C32 = gpu["C"][t].astype(np.float32)
     idx_ref = O.hard_assign(w, C32)
@@ -310,7 +332,10 @@ def test_host_pipeline_matches_oracle():
     dC = torch.cat([d.cpu() for d in dC]).numpy()
     for t in range(len(sizes)):
         ref = oracle_dense(bits_of(Ws[t]), Gs[t].double().numpy(), C0[t].cpu().numpy(), p)
-        assert np.all(np.abs(as16_values(hWt[t]) - ref["Wt"]) <= ulp16(ref["Wt"], torch.bfloat16))
+        if np.min(ref["St"]) < 1e-6 * sizes[t]:
+            continue  # dead cluster: parity unpinned (R6)
+        assert np.all(np.abs(as16_values(hWt[t]) - ref["Wt"]) <= ulp16(ref["Wt"], torch.bfloat16)
+                      + TOL * np.max(np.abs(ref["Wt"])))
         lim = ulp16(ref["dW"], torch.bfloat16) + TOL * np.max(np.abs(ref["dW"]))
         assert np.all(np.abs(as16_values(hdW[t]) - ref["dW"]) <= lim)
         assert np.max(np.abs(dC[t] - ref["dC"])) <= TOL * np.max(np.abs(ref["dC"])) + 1e-37
