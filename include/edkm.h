@@ -21,7 +21,7 @@
  *     allocates no device memory and keeps no state between calls.
  *   - Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
  *     default stream).  No call synchronises the host except edkm_read_status.
- *   - Argument errors (null pointers with n > 0, bad dtype, bits outside 1..4,
+ *   - Argument errors (null pointers with n > 0, bad dtype, bits outside 1..8,
  *     tau <= 0 or non-finite, max_iter < 0, eps < 0 or NaN, nt < 0, n < 0) are
  *     returned before anything is launched and have no side effects.
  *   - Launch failures return EDKM_E_CUDA; edkm_last_error() gives the text.
@@ -66,7 +66,7 @@ typedef struct {
 
 typedef struct {
     int wdtype;    /* EDKM_BF16 or EDKM_FP16: the weights' 16-bit format   */
-    int bits;      /* b, 1..4 in this build; k = 2^b centroids        */
+    int bits;      /* b, 1..8; k = 2^b centroids (8-bit embeddings P:91)    */
     double tau;    /* softmax temperature, > 0 and finite                         */
     int max_iter;  /* >= 0: number of centroid updates when eps == 0 (DESIGN R3)   */
     double eps;    /* >= 0; if > 0 stop once max_j |C_{t+1}[j]-C_t[j]| <= eps (R4) */

@@ -37,7 +37,7 @@ int sm_count() {
 bool params_ok(const edkm_params* p) {
   if (!p) return false;
   if (p->wdtype != EDKM_BF16 && p->wdtype != EDKM_FP16) return false;
-  if (p->bits < 1 || p->bits > 4) return false;
+  if (p->bits < 1 || p->bits > 8) return false;
   if (!(p->tau > 0.0) || !isfinite(p->tau)) return false;
   if (p->max_iter < 0 || p->max_iter > 100000) return false;
   if (!(p->eps >= 0.0) || !isfinite(p->eps)) return false;
@@ -47,7 +47,7 @@ bool params_ok(const edkm_params* p) {
 edkm_status check_params(const edkm_params* p) {
   if (!p) return fail(EDKM_E_ARG, "params is NULL");
   if (p->wdtype != EDKM_BF16 && p->wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");
-  if (p->bits < 1 || p->bits > 4) return fail(EDKM_E_UNSUPPORTED, "bits must be in 1..4 in this build");
+  if (p->bits < 1 || p->bits > 8) return fail(EDKM_E_UNSUPPORTED, "bits must be in 1..8");
   if (!params_ok(p)) return fail(EDKM_E_ARG, "tau must be > 0 and finite, max_iter in [0, 1e5], eps >= 0 and finite");
   return EDKM_OK;
 }
@@ -195,7 +195,7 @@ edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, co
   P.C0 = C0;
   P.C_out = C_out;
   P.table = table;
-  cudaError_t e = launch_tf(P, (cudaStream_t)stream);
+  cudaError_t e = P.k >= 32 ? launch_tf_wide(P, (cudaStream_t)stream) : launch_tf(P, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "TF table-forward launch");
   g_launches = 1;
   return EDKM_OK;
@@ -270,7 +270,7 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
   const int sms = sm_count();
   e = for_groups(tensors, nt, grads, nullptr, A, [&](const StreamArgs& a) { return launch_b1(a, Bq, sms, s); });
   if (e != cudaSuccess) return cuda_fail(e, "B1 bucket launch");
-  e = launch_tgamma(P, s);
+  e = P.k >= 32 ? launch_tgamma_wide(P, s) : launch_tgamma(P, s);
   if (e != cudaSuccess) return cuda_fail(e, "TGAMMA launch");
   ++g_launches;
   return EDKM_OK;
@@ -298,7 +298,7 @@ edkm_status edkm_backward_apply(const edkm_tensor* tensors, int nt, const edkm_p
   P.counts = counts;
   P.gamma = const_cast<double*>(gamma);
   P.dC0 = dC0;
-  cudaError_t e = launch_tb(P, s);
+  cudaError_t e = P.k >= 32 ? launch_tb_wide(P, s) : launch_tb(P, s);
   if (e != cudaSuccess) return cuda_fail(e, "TB table-backward launch");
   ++g_launches;
   B2Args Bq;

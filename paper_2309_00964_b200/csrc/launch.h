@@ -74,5 +74,9 @@ int table_cluster_size(int nt);
 cudaError_t launch_tf(const TableArgs& P, cudaStream_t s);
 cudaError_t launch_tgamma(const TableArgs& P, cudaStream_t s);
 cudaError_t launch_tb(const TableArgs& P, cudaStream_t s);
+// k = 32..256 (bits 5..8): warp-per-row variants (table_wide.cu)
+cudaError_t launch_tf_wide(const TableArgs& P, cudaStream_t s);
+cudaError_t launch_tgamma_wide(const TableArgs& P, cudaStream_t s);
+cudaError_t launch_tb_wide(const TableArgs& P, cudaStream_t s);
 
 }  // namespace edkm

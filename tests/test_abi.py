@@ -52,8 +52,10 @@ def test_bad_arguments_return_errors_without_launch(L):
                 E._Params(0, 3, 1.0, 5, -1.0), E._Params(0, 3, float("inf"), 5, 0.0)):
         assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(bad), ctypes.c_void_p(16), ctypes.c_void_p(16),
                               ctypes.c_void_p(16), ctypes.c_void_p(16), None) == 1
-    assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(0, 5, 1.0, 5, 0.0)), None, None, None, None,
-                          None) == 4                              # bits > 4: unsupported in this build
+    assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(0, 9, 1.0, 5, 0.0)), None, None, None, None,
+                          None) == 4                              # bits > 8: unsupported
+    assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(0, 0, 1.0, 5, 0.0)), None, None, None, None,
+                          None) == 4                              # bits < 1
     assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(E._Params(2, 3, 1.0, 5, 0.0)), None, None, None, None,
                           None) == 2                              # fp32 weights
     assert L.edkm_forward(None, 1, cp, None, None, None, None, None) == 1

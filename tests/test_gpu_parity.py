@@ -175,6 +175,11 @@ def test_cfg1_full_parity():
     (torch.float16, 4, 1e-5, 30, 0.02, 200_000),
     (torch.float16, 2, 1e-5, 30, 0.02, 120_007),
     (torch.float16, 3, 1e-3, 5, 1.0, 131_075),
+    # bits 5..8 (warp-per-row table kernels; 8-bit embeddings)
+    (torch.bfloat16, 5, 1e-3, 4, 1.0, 300_000),
+    (torch.bfloat16, 6, 2e-6, 3, 0.02, 200_001),
+    (torch.float16, 7, 1e-4, 3, 1.0, 150_000),
+    (torch.bfloat16, 8, 1e-8, 3, 0.02, 400_000),
 ])
 def test_parity_sweep(dtype, bits, tau, T, sigma, n):
     k = 1 << bits
