@@ -33,21 +33,21 @@ constexpr int kTWarps = kTThreads / 32;
 constexpr int kStage = 6144;  // rows per CTA staged in shared memory (v, n, psi: 24 B each)
 constexpr size_t kStageBytes = (size_t)kStage * 24;
 
-// Centroids of one iteration in the forms the attention needs: fp64 values, a float-float
-// split (hi + lo), and per centroid pair (m, j) the fp64-derived difference C_m - C_j
-// (fp32) and sum C_m + C_j (float-float).
+// Centroids of one iteration in the forms the attention needs: fp64 values, fp32 values
+// (to pick the nearest centroid), and per centroid pair (m, j) the fp64-derived difference
+// (C_m - C_j) / tau * log2(e) (fp32) and sum C_m + C_j (float-float ph + pl).
 template <int K>
 struct CSet {
   double c[K];
-  float hi[K], lo[K];
-  float dm[K][K];          // C_m - C_j
-  float ph[K][K], pl[K][K];  // C_m + C_j = ph + pl
+  float hi[K];
+  float dms[K][K];
+  float ph[K][K], pl[K][K];
   // every thread of the block calls it; the caller synchronises before and after
-  __device__ void prepare(const double* src) {
+  __device__ void prepare(const double* src, double inv_tau) {
     const int t = threadIdx.x;
     if (t < K * K) {
       const double a = src[t / K], b = src[t % K], p = a + b;
-      dm[t / K][t % K] = (float)(a - b);
+      dms[t / K][t % K] = (float)((a - b) * inv_tau * 1.4426950408889634);
       const float h = (float)p;
       ph[t / K][t % K] = h;
       pl[t / K][t % K] = (float)(p - (double)h);
@@ -55,50 +55,46 @@ struct CSet {
     if (t < K) {
       c[t] = src[t];
       hi[t] = (float)src[t];
-      lo[t] = (float)(src[t] - (double)hi[t]);
     }
   }
 };
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // DKM attention of one pattern value v (exact in fp32: a 16-bit float) to the K centroids:
 //   A_j = exp(-(d_j - d_min)/tau) / sum_l exp(-(d_l - d_min)/tau),  d_j = (v - C_j)^2.
-// With m = argmin_j |v - C_j|, d_j - d_m = (C_m - C_j)(2v - C_m - C_j).  The second factor
+// With m the nearest centroid, d_j - d_m = (C_m - C_j)(2v - C_m - C_j).  The second factor
 // is 2v - (ph + pl) in fp32: exact where it is small (2v and ph within a factor 2,
-// Sterbenz), so near a cluster boundary -- where A is most sensitive -- the logit carries
-// relative, not absolute, fp32 error (~1e-7).  exp(-x) = 2^-y is split as 2^-f * 2^-n
-// (n = floor y): 2^-f in fp32 (MUFU), 2^-n applied exactly in fp64, so tiny weights keep
-// the range of fp64 exp.  A is returned normalised in fp64; callers sum in fp64 (R7).
+// Sterbenz), so near a cluster boundary -- where A is most sensitive -- the logit carries a
+// relative, not absolute, fp32 error (~1e-7); far from it the weight is tiny.  The
+// exponential is MUFU ex2 (rel. error ~2^-22); A is normalised in fp32 and every sum over
+// patterns is done by the callers in fp64 (R7).
 template <int K>
-__device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float sc, double (&A)[K]) {
+__device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float (&A)[K]) {
   int jm = 0;
-  float am = INFINITY;
+  float am = fabsf(vf - cs.hi[0]);
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const float a = fabsf((vf - cs.hi[j]) - cs.lo[j]);
+  for (int j = 1; j < K; ++j) {
+    const float a = fabsf(vf - cs.hi[j]);
     if (a < am) { am = a; jm = j; }
   }
-  const float* dmr = cs.dm[jm];
+  const float* dmr = cs.dms[jm];
   const float* phr = cs.ph[jm];
   const float* plr = cs.pl[jm];
   const float v2 = 2.0f * vf;
-  float a[K];
-  int nexp[K];
   float Z = 0.0f;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const float s = (v2 - phr[j]) - plr[j];
-    const float y = (dmr[j] * s) * sc;  // >= ~0: exponent in base 2
-    const float n = floorf(y);
-    nexp[j] = (int)n;
-    a[j] = exp2f(n - y);                               // 2^-f, in (0.5, 1]
-    Z += nexp[j] < 126 ? __int_as_float((127 - nexp[j]) << 23) * a[j] : 0.0f;  // fp32 is enough for Z >= ~1
+    A[j] = ex2(-(dmr[j] * ((v2 - phr[j]) - plr[j])));
+    Z += A[j];
   }
   const float iz = 1.0f / Z;
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const double p2 = nexp[j] > 1022 ? 0.0 : __longlong_as_double((long long)(1023 - nexp[j]) << 52);  // 2^-n
-    A[j] = (double)(a[j] * iz) * p2;
-  }
+  for (int j = 0; j < K; ++j) A[j] *= iz;
 }
 
 // Sum N doubles over the CTA then over the cluster; result in tot[0..N) of every CTA.
@@ -264,22 +260,21 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     if (crank == 0) ctraj[tid] = sC[tid];
   }
   __syncthreads();
-  const float sc = (float)(P.inv_tau * 1.4426950408889634);  // 1/tau in exp2 units
   int T = P.max_iter;
   for (int it = 0; it < P.max_iter; ++it) {
-    cs.prepare(sC);
+    cs.prepare(sC, P.inv_tau);
     __syncthreads();
     double acc[2 * K];
 #pragma unroll
     for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
     for (int r = tid; r < nr; r += kTThreads) {
       const double v = R.v(r), n = R.n(r), nv = n * v;
-      double A[K];
-      attention_row<K>((float)v, cs, sc, A);
+      float A[K];
+      attention_row<K>((float)v, cs, A);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        acc[j] = fma(A[j], n, acc[j]);
-        acc[K + j] = fma(A[j], nv, acc[K + j]);
+        acc[j] = fma((double)A[j], n, acc[j]);
+        acc[K + j] = fma((double)A[j], nv, acc[K + j]);
       }
     }
     cluster_allreduce<2 * K>(acc, red, part, tot, it & 1, cluster);
@@ -310,7 +305,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     if (crank == 0) P.C_out[(int64_t)t * K + tid] = cf;
     sCf[tid] = (double)cf;  // the deployable fp32 lookup table (R9)
   }
-  cs.prepare(sC);
+  cs.prepare(sC, P.inv_tau);
   __syncthreads();
 
   // ---- 3. per populated pattern: W~ (fp32 and 16-bit), hard index vs the fp32 C_out
@@ -325,11 +320,11 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
       if (d < bd) { bd = d; best = j; }
     }
     idx[u] = (uint8_t)best;
-    double A[K];
-    attention_row<K>((float)v, cs, sc, A);
+    float A[K];
+    attention_row<K>((float)v, cs, A);
     double wt = 0.0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) wt = fma(A[j], cs.c[j], wt);
+    for (int j = 0; j < K; ++j) wt = fma((double)A[j], cs.c[j], wt);
     tab[u] = (float)wt;
     tab16[u] = round16(wt, P.wdtype);
   }
@@ -345,10 +340,9 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
   __shared__ CSet<K> cs;
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
-  cs.prepare(P.ctraj + (int64_t)t * (P.max_iter + 1) * K + (int64_t)T * K);
+  cs.prepare(P.ctraj + (int64_t)t * (P.max_iter + 1) * K + (int64_t)T * K, P.inv_tau);
   __syncthreads();
   const double* sC = cs.c;
-  const float sc = (float)(P.inv_tau * 1.4426950408889634);
   const double* Bt = P.B + (int64_t)t * kPatterns;
   double acc[K];
 #pragma unroll
@@ -361,10 +355,14 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
       const double B = Bt[u];
       if (B == 0.0) continue;
       const double v = decode16(u, P.wdtype);
+      float Af[K];
+      attention_row<K>((float)v, cs, Af);
       double A[K], wt = 0.0;
-      attention_row<K>((float)v, cs, sc, A);
 #pragma unroll
-      for (int l = 0; l < K; ++l) wt = fma(A[l], sC[l], wt);
+      for (int l = 0; l < K; ++l) {
+        A[l] = (double)Af[l];
+        wt = fma(A[l], sC[l], wt);
+      }
 #pragma unroll
       for (int l = 0; l < K; ++l) acc[l] += B * A[l] * (1.0 + (sC[l] - wt) * 2.0 * (v - sC[l]) * P.inv_tau);
     }
@@ -380,10 +378,9 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double sG[K], sCn[K], sInvS[K], red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[kTWarps * K], part[2 * K], tot[K];
   __shared__ CSet<K> cs;
   const double* sCt = cs.c;
-  const float sc = (float)(P.inv_tau * 1.4426950408889634);
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
@@ -399,12 +396,18 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
+  const double h1 = 2.0 * P.inv_tau;
   for (int it = T - 1; it >= 0; --it) {
-    cs.prepare(ctraj + (int64_t)it * K);
+    cs.prepare(ctraj + (int64_t)it * K, P.inv_tau);
     if (tid < K) {
-      sCn[tid] = ctraj[(int64_t)(it + 1) * K + tid];
+      // per-iteration constants: gh_j = g1_j v - g2_j, dz_l = h1 v - h2_l
+      const double cn = ctraj[(int64_t)(it + 1) * K + tid];
       const double S = straj[(int64_t)it * K + tid];
-      sInvS[tid] = S != 0.0 ? 1.0 / S : 0.0;
+      const double is = S != 0.0 ? 1.0 / S : 0.0;
+      sInvS[tid] = is;
+      sG1[tid] = sG[tid] * is;
+      sG2[tid] = sG[tid] * cn * is;
+      sH2[tid] = h1 * ctraj[(int64_t)it * K + tid];
     }
     __syncthreads();
     double acc[K];
@@ -417,21 +420,23 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       for (int r = tid; r < nr; r += kTThreads) {
         const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
         const double n = one ? R.n(r) : (double)cnt[rows[r]];
+        float Af[K];
+        attention_row<K>((float)v, cs, Af);
         double A[K], gh[K];
-        attention_row<K>((float)v, cs, sc, A);
         double s = 0.0, dpsi = 0.0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          gh[j] = sG[j] * (v - sCn[j]) * sInvS[j];  // dL/dA_t[u][j] (zero where S_t[j] = 0)
-          s += A[j] * gh[j];
-          dpsi += sG[j] * A[j] * sInvS[j];           // direct path of v through M_t
+          A[j] = (double)Af[j];
+          gh[j] = fma(sG1[j], v, -sG2[j]);           // dL/dA_t[u][j] (zero where S_t[j] = 0)
+          s = fma(A[j], gh[j], s);
+          dpsi = fma(A[j], sG1[j], dpsi);             // direct path of v through M_t
         }
 #pragma unroll
         for (int l = 0; l < K; ++l) {
           const double rr = A[l] * (gh[l] - s);      // softmax Jacobian applied to gh
-          const double dz = 2.0 * (v - sCt[l]) * P.inv_tau;
-          dpsi -= rr * dz;
-          acc[l] += n * rr * dz;
+          const double q = rr * fma(h1, v, -sH2[l]);  // rr * dz_l, dz_l = 2 (v - C_t[l]) / tau
+          dpsi -= q;
+          acc[l] = fma(n, q, acc[l]);
         }
         double& ps = one ? R.psi(r) : gpsi[r];
         ps = (it == T - 1 ? 0.0 : ps) + dpsi;
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   }
   if (crank == 0 && tid < K) P.dC0[(int64_t)t * K + tid] = (float)sG[tid];
   // (phi, psi) table: phi[u] = (2/tau) sum_l A_T[u,l] (C_T[l] - W~_u)^2
-  cs.prepare(ctraj + (int64_t)T * K);
+  cs.prepare(ctraj + (int64_t)T * K, P.inv_tau);
   __syncthreads();
   float2* pp = P.phipsi + (int64_t)t * kPatterns;
   for (int p = crank; p < pcl; p += cl) {
@@ -453,14 +458,14 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
     for (int r = tid; r < nr; r += kTThreads) {
       const uint32_t u = rows[r];
       const double v = one ? R.v(r) : decode16(u, P.wdtype);
-      double A[K];
-      attention_row<K>((float)v, cs, sc, A);
+      float Af[K];
+      attention_row<K>((float)v, cs, Af);
       double wt = 0.0;
 #pragma unroll
-      for (int l = 0; l < K; ++l) wt = fma(A[l], sCt[l], wt);
+      for (int l = 0; l < K; ++l) wt = fma((double)Af[l], sCt[l], wt);
       double var = 0.0;
 #pragma unroll
-      for (int l = 0; l < K; ++l) var += A[l] * (sCt[l] - wt) * (sCt[l] - wt);
+      for (int l = 0; l < K; ++l) var += (double)Af[l] * (sCt[l] - wt) * (sCt[l] - wt);
       const double ps = T > 0 ? (one ? R.psi(r) : gpsi[r]) : 0.0;
       pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
     }
