@@ -205,9 +205,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     uint4* h4 = reinterpret_cast<uint4*>(tab16 + u0);
     h4[0] = make_uint4(n16, n16, n16, n16);
     h4[1] = make_uint4(n16, n16, n16, n16);
-    if (!pattern_finite(u0, P.wdtype) || !pattern_finite(u0 + 15, P.wdtype))
-      for (int e = 0; e < 16; ++e)
-        if (!pattern_finite(u0 + e, P.wdtype)) idx[u0 + e] = 0;
+    *reinterpret_cast<uint4*>(idx + u0) = make_uint4(0, 0, 0, 0);  // populated entries set in phase 3
     // one signed page = 256 patterns = 16 threads
 #pragma unroll
     for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
@@ -469,9 +467,10 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       const double ps = T > 0 ? (one ? R.psi(r) : gpsi[r]) : 0.0;
       pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
     }
-    // NaN/Inf patterns: dW = NaN (R10)
+    // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN
     for (int u = p * chunk + tid; u < (p + 1) * chunk; u += kTThreads)
-      if (!pattern_finite(u, P.wdtype)) pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+      if (!pattern_finite(u, P.wdtype) || cnt[u] == 0)
+        pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
   }
   cluster.sync();
 }

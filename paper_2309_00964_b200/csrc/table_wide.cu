@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
     const int c = cnt[u];
     const bool fin = pattern_finite(u, P.wdtype);
     const bool pop = fin && c > 0;
-    if (!fin) { nonfin += c; idx[u] = 0; }
+    if (!fin) nonfin += c;
+    idx[u] = 0;  // populated entries set in phase 3
     tab[u] = nanf;
     tab16[u] = nan16(P.wdtype);
     const unsigned b = __ballot_sync(0xffffffffu, pop);
@@ -437,7 +438,8 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
       }
     }
     for (int u = p * chunk + tid; u < (p + 1) * chunk; u += kWThreads)
-      if (!pattern_finite(u, P.wdtype)) pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+      if (!pattern_finite(u, P.wdtype) || cnt[u] == 0)
+        pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
   }
   cluster.sync();
 }
