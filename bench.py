@@ -213,12 +213,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # under torchrun: always use the process group
+    distributed = world > 1 or launched
+    if distributed:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         B.build()
-    if world > 1:
+    if distributed:
         dist.barrier()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -243,7 +245,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def allreduce(t):
-        if world > 1:
+        if distributed:
             dist.all_reduce(t)
 
     def step(ev=None):
@@ -272,7 +274,7 @@ def main():
     # per-phase events in every timed step (same stream as the kernels)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -281,14 +283,14 @@ def main():
             step(evs[s])
         stop.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     ms = start.elapsed_time(stop) / args.steps
     names = ["F1", "AR_counts", "TF", "F2", "B1+TG", "AR_gamma", "TB+B2"]
     phase = {n: sum(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)) / args.steps
              for i, n in enumerate(names)}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     launches_per_step = 7
@@ -307,7 +309,7 @@ def main():
         torch.cuda.synchronize()
 
         from paper_2309_00964_b200.pipeline import HostPipeline
-        pipe = HostPipeline(numels, p, dev, n_groups=8, allreduce=allreduce if world > 1 else None,
+        pipe = HostPipeline(numels, p, dev, n_groups=8, allreduce=allreduce if distributed else None,
                             buffers=(Ws, Gs, Wt, dW))
 
         def e2e_step():
@@ -315,7 +317,7 @@ def main():
 
         e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -324,7 +326,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         bytes_in = sum(w.numel() * 2 + g.numel() * 2 for w, g in zip(Ws, Gs))
         bytes_out = sum(w.numel() * 2 * 2 for w in Ws)
@@ -334,7 +336,7 @@ def main():
         del hW, hG, hWt, hdW
 
     if rank != 0:
-        if world > 1:
+        if distributed:
             dist.destroy_process_group()
         return
 
@@ -367,7 +369,7 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)
     print(json.dumps(out))
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

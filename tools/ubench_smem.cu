@@ -60,7 +60,7 @@ __global__ void k_read(const uint4* w, size_t n16, uint32_t* out) {
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k_hist(const uint4* w, size_t n16, uint32_t* gout) {
   extern __shared__ uint32_t h[];
-  const int nw = (MODE == 3) ? 16384 : (MODE >= 10 ? 57344 : 32768);
+  const int nw = (MODE == 3) ? 16384 : ((MODE >= 10 || MODE == 5) ? 57344 : 32768);
   for (int i = threadIdx.x; i < nw; i += blockDim.x) h[i] = 0;
   __syncthreads();
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -84,6 +84,10 @@ __global__ void __launch_bounds__(1024, 1) k_hist(const uint4* w, size_t n16, ui
           uint32_t a = (uint32_t)__cvta_generic_to_shared(&h[u >> 1]);
           if (u & 1u) asm volatile("red.shared.add.u32 [%0], 65536;" :: "r"(a));
           else asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(a));
+        } else if (MODE == 5) {  // u32 atom with return, result consumed cheaply
+          uint32_t old;
+          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"((uint32_t)__cvta_generic_to_shared(&h[u % 57344u])));
+          spill ^= old;
         } else if (MODE >= 10) {  // C = MODE-10 copies interleaved: word = idx*C + lane%C, idx in [0, 224K/4/C)
           constexpr int C = MODE - 10;
           const uint32_t idx = u % (57344u / C);
@@ -195,6 +199,8 @@ int main() {
   run("hist 1/2 L2 red", [&] { k_hist_l2<2><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
   run("hist 1/4 L2 red", [&] { k_hist_l2<4><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
   run("hist 1/8 L2 red", [&] { k_hist_l2<8><<<sms, 1024, 229376>>>((const uint4*)w, n16, gcnt, o); }, n * 2.0);
+  cudaFuncSetAttribute(k_hist<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 229376);
+  run("hist u32 atom+ret (xor)", [&] { k_hist<5><<<sms, 1024, 229376>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("hist u32 32K red", [&] { k_hist<2><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom", [&] { k_hist<3><<<sms, 1024, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom 3x/SM", [&] { k_hist<3><<<sms * 3, 1024 / 2, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
