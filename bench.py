@@ -29,7 +29,6 @@ sys.path.insert(0, ROOT)
 METRIC = "DKM fwd+bwd weights/sec (LLaMA-7B, 3-bit) at 1/2/4/8 B200; % HBM peak"
 # algorithmic HBM bytes per weight of each per-weight pass (S4), bf16 I/O
 BYTES_PER_WEIGHT = {"F1": 2, "F2": 4, "B1": 4, "B2": 6}
-PHASES = ["F1", "AR_counts", "TF", "F2", "B1+TG", "AR_gamma", "TB", "B2"]
 
 
 def parse():
@@ -249,30 +248,35 @@ def main():
             dist.all_reduce(t)
 
     def step(ev=None):
+        # the seven kernels of the hot path, one C-ABI call each, events between them
         def mark(i):
             if ev is not None:
                 ev[i].record(stream)
         mark(0)
-        plan.uniquify(Ws)
+        plan.uniquify(Ws)                    # F1
         mark(1)
-        allreduce(plan.counts)
+        allreduce(plan.counts)               # exchange 1 (N > 1)
         mark(2)
-        plan.forward(C0)
+        plan.forward(C0)                     # TF
         mark(3)
-        plan.reconstruct(Ws, Wt, E.SOFT)
+        plan.reconstruct(Ws, Wt, E.SOFT)     # F2
         mark(4)
-        plan.backward_reduce(Ws, Gs)
+        plan.backward_buckets(Ws, Gs)        # B1
         mark(5)
-        allreduce(plan.gamma)
+        plan.backward_gamma()                # TGAMMA
         mark(6)
-        plan.backward_apply(Ws, Gs, dW)
+        allreduce(plan.gamma)                # exchange 2 (N > 1)
         mark(7)
+        plan.backward_table()                # TB
+        mark(8)
+        plan.backward_dw(Ws, Gs, dW)         # B2
+        mark(9)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # per-phase events in every timed step (same stream as the kernels)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(10)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if distributed:
         dist.barrier()
@@ -286,7 +290,7 @@ def main():
     if distributed:
         dist.barrier()
     ms = start.elapsed_time(stop) / args.steps
-    names = ["F1", "AR_counts", "TF", "F2", "B1+TG", "AR_gamma", "TB+B2"]
+    names = ["F1", "AR_counts", "TF", "F2", "B1", "TGAMMA", "AR_gamma", "TB", "B2"]
     phase = {n: sum(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)) / args.steps
              for i, n in enumerate(names)}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -342,9 +346,9 @@ def main():
 
     # ---- roofline of the dominant per-weight kernel (measured live above)
     peak, peak_src = measured_peaks()
-    per_kernel = {"F1": phase["F1"], "F2": phase["F2"], "B1+TG": phase["B1+TG"], "TB+B2": phase["TB+B2"]}
+    per_kernel = {k: phase[k] for k in ("F1", "F2", "B1", "B2")}
     dom = max(per_kernel, key=per_kernel.get)
-    key = {"F1": "F1", "F2": "F2", "B1+TG": "B1", "TB+B2": "B2"}[dom]
+    key = dom
     alg = BYTES_PER_WEIGHT[key] * n_local
     achieved = alg / (per_kernel[dom] / 1e3) / 1e9
     tr = ncu_traffic(key)

@@ -130,6 +130,22 @@ edkm_status edkm_backward_apply(const edkm_tensor* tensors, int nt, const edkm_p
                                 const void* saved, void* ws, const double* gamma, void* const* dW,
                                 int dw_dtype, float* dC0, void* stream);
 
+/* The four kernels of the two calls above, individually (same semantics; for overlap or
+ * per-kernel timing):
+ *   edkm_backward_buckets : B1     -- ws buckets B[u] of this rank's slice (zeroed first)
+ *   edkm_backward_gamma   : TGAMMA -- gamma (this rank's partial) from the buckets
+ *   edkm_backward_table   : TB     -- (phi, psi) per pattern into ws, dC0, from the global gamma
+ *   edkm_backward_dw      : B2     -- dW from (phi, psi) */
+edkm_status edkm_backward_buckets(const edkm_tensor* tensors, int nt, const edkm_params* p,
+                                  const void* const* grads, int gdtype, const void* saved, void* ws, void* stream);
+edkm_status edkm_backward_gamma(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
+                                double* gamma, void* stream);
+edkm_status edkm_backward_table(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
+                                const double* gamma, float* dC0, void* stream);
+edkm_status edkm_backward_dw(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                             int gdtype, const void* saved, const void* ws, void* const* dW, int dw_dtype,
+                             void* stream);
+
 /* Single-process convenience: edkm_backward_reduce then edkm_backward_apply with
  * `gamma` in ws.  Only valid when one process holds every weight of each tensor. */
 edkm_status edkm_backward(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,

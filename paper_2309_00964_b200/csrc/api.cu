@@ -241,10 +241,8 @@ edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_para
   return EDKM_OK;
 }
 
-edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
-                                 int gdtype, const int32_t* counts, const void* saved, void* ws, double* gamma,
-                                 void* stream) {
-  g_launches = 0;
+static edkm_status check_backward(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                                  int gdtype) {
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
   st = check_tensors(tensors, nt);
@@ -252,13 +250,19 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
   st = check_ptrs(grads, tensors, nt, "grads");
   if (st != EDKM_OK) return st;
   if (gdtype != p->wdtype && gdtype != EDKM_FP32) return fail(EDKM_E_DTYPE, "grads must be the weights' dtype or FP32");
+  return EDKM_OK;
+}
+
+edkm_status edkm_backward_buckets(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                                  int gdtype, const void* saved, void* ws, void* stream) {
+  g_launches = 0;
+  edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
+  if (st != EDKM_OK) return st;
   if (nt == 0) return EDKM_OK;
-  if (!counts || !saved || !ws || !gamma) return fail(EDKM_E_ARG, "NULL buffer");
+  if (!saved || !ws) return fail(EDKM_E_ARG, "NULL buffer");
   cudaStream_t s = (cudaStream_t)stream;
   TableArgs P = table_args(nt, p, saved);
   ws_args(P, ws);
-  P.counts = counts;
-  P.gamma = gamma;
   cudaError_t e = cudaMemsetAsync((void*)P.B, 0, (size_t)nt * kPatterns * sizeof(double), s);
   if (e != cudaSuccess) return cuda_fail(e, "memset buckets");
   B1Args Bq;
@@ -270,37 +274,75 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
   const int sms = sm_count();
   e = for_groups(tensors, nt, grads, nullptr, A, [&](const StreamArgs& a) { return launch_b1(a, Bq, sms, s); });
   if (e != cudaSuccess) return cuda_fail(e, "B1 bucket launch");
-  e = P.k >= 32 ? launch_tgamma_wide(P, s) : launch_tgamma(P, s);
-  if (e != cudaSuccess) return cuda_fail(e, "TGAMMA launch");
-  ++g_launches;
   return EDKM_OK;
 }
 
-edkm_status edkm_backward_apply(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
-                                int gdtype, const int32_t* counts, const void* saved, void* ws, const double* gamma,
-                                void* const* dW, int dw_dtype, float* dC0, void* stream) {
+edkm_status edkm_backward_gamma(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
+                                double* gamma, void* stream) {
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
-  st = check_tensors(tensors, nt);
+  if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
+  if (nt == 0) return EDKM_OK;
+  if (!counts || !saved || !ws || !gamma) return fail(EDKM_E_ARG, "NULL buffer");
+  TableArgs P = table_args(nt, p, saved);
+  ws_args(P, ws);
+  P.counts = counts;
+  P.gamma = gamma;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = P.k >= 32 ? launch_tgamma_wide(P, s) : launch_tgamma(P, s);
+  if (e != cudaSuccess) return cuda_fail(e, "TGAMMA launch");
+  g_launches = 1;
+  return EDKM_OK;
+}
+
+edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                                 int gdtype, const int32_t* counts, const void* saved, void* ws, double* gamma,
+                                 void* stream) {
+  edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
   if (st != EDKM_OK) return st;
-  st = check_ptrs(grads, tensors, nt, "grads");
+  if (nt > 0 && (!counts || !gamma)) return fail(EDKM_E_ARG, "NULL buffer");
+  st = edkm_backward_buckets(tensors, nt, p, grads, gdtype, saved, ws, stream);
   if (st != EDKM_OK) return st;
-  st = check_ptrs(dW, tensors, nt, "dW");
+  const int n1 = g_launches;
+  st = edkm_backward_gamma(nt, p, counts, saved, ws, gamma, stream);
+  if (st == EDKM_OK) g_launches += n1;
+  return st;
+}
+
+edkm_status edkm_backward_table(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
+                                const double* gamma, float* dC0, void* stream) {
+  g_launches = 0;
+  edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
-  if (gdtype != p->wdtype && gdtype != EDKM_FP32) return fail(EDKM_E_DTYPE, "grads must be the weights' dtype or FP32");
-  if (dw_dtype != p->wdtype && dw_dtype != EDKM_FP32) return fail(EDKM_E_DTYPE, "dW must be the weights' dtype or FP32");
+  if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
   if (nt == 0) return EDKM_OK;
   if (!counts || !saved || !ws || !gamma || !dC0) return fail(EDKM_E_ARG, "NULL buffer");
-  cudaStream_t s = (cudaStream_t)stream;
   TableArgs P = table_args(nt, p, saved);
   ws_args(P, ws);
   P.counts = counts;
   P.gamma = const_cast<double*>(gamma);
   P.dC0 = dC0;
+  cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = P.k >= 32 ? launch_tb_wide(P, s) : launch_tb(P, s);
   if (e != cudaSuccess) return cuda_fail(e, "TB table-backward launch");
-  ++g_launches;
+  g_launches = 1;
+  return EDKM_OK;
+}
+
+edkm_status edkm_backward_dw(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                             int gdtype, const void* saved, const void* ws, void* const* dW, int dw_dtype,
+                             void* stream) {
+  g_launches = 0;
+  edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
+  if (st != EDKM_OK) return st;
+  st = check_ptrs(dW, tensors, nt, "dW");
+  if (st != EDKM_OK) return st;
+  if (dw_dtype != p->wdtype && dw_dtype != EDKM_FP32) return fail(EDKM_E_DTYPE, "dW must be the weights' dtype or FP32");
+  if (nt == 0) return EDKM_OK;
+  if (!saved || !ws) return fail(EDKM_E_ARG, "NULL buffer");
+  TableArgs P = table_args(nt, p, saved);
+  ws_args(P, const_cast<void*>(ws));
   B2Args Bq;
   Bq.phipsi = P.phipsi;
   Bq.page_cnt = P.page_cnt;
@@ -309,9 +351,26 @@ edkm_status edkm_backward_apply(const edkm_tensor* tensors, int nt, const edkm_p
   A.gdtype = gdtype;
   A.odtype = dw_dtype;
   const int sms = sm_count();
-  e = for_groups(tensors, nt, grads, dW, A, [&](const StreamArgs& a) { return launch_b2(a, Bq, sms, s); });
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = for_groups(tensors, nt, grads, dW, A, [&](const StreamArgs& a) { return launch_b2(a, Bq, sms, s); });
   if (e != cudaSuccess) return cuda_fail(e, "B2 dW launch");
   return EDKM_OK;
+}
+
+edkm_status edkm_backward_apply(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
+                                int gdtype, const int32_t* counts, const void* saved, void* ws, const double* gamma,
+                                void* const* dW, int dw_dtype, float* dC0, void* stream) {
+  edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
+  if (st != EDKM_OK) return st;
+  st = check_ptrs(dW, tensors, nt, "dW");
+  if (st != EDKM_OK) return st;
+  if (dw_dtype != p->wdtype && dw_dtype != EDKM_FP32) return fail(EDKM_E_DTYPE, "dW must be the weights' dtype or FP32");
+  st = edkm_backward_table(nt, p, counts, saved, ws, gamma, dC0, stream);
+  if (st != EDKM_OK) return st;
+  const int n1 = g_launches;
+  st = edkm_backward_dw(tensors, nt, p, grads, gdtype, saved, ws, dW, dw_dtype, stream);
+  if (st == EDKM_OK) g_launches += n1;
+  return st;
 }
 
 edkm_status edkm_backward(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,

@@ -9,8 +9,8 @@ Entry points (same names as the C ABI; PAPER.md = /root/reference/PAPER.md):
   uniquify          F1: counts per 16-bit pattern (Fig. 3)
   forward           TF: unrolled DKM iterations on the attention table
   reconstruct       F2: W~ = table[bits(w)] / hard palettisation (Fig. 1)
-  backward_reduce   B1 + gamma_T partial
-  backward_apply    TB + B2: dC_0 and dW
+  backward_reduce   B1 + gamma_T partial   (= backward_buckets + backward_gamma)
+  backward_apply    TB + B2: dC_0 and dW   (= backward_table + backward_dw)
   backward          both (single process)
 ``Plan`` owns the per-step buffers (counts, saved, ws, ...) so a training step
 allocates nothing; ``EDKMFunction`` wraps one tensor as a torch.autograd.Function.
@@ -68,6 +68,10 @@ def lib():
             "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P], i32),
             "edkm_backward_apply": ([P, i32, pp, P, i32, P, P, P, P, P, i32, P, P], i32),
             "edkm_backward": ([P, i32, pp, P, i32, P, P, P, P, i32, P, P], i32),
+            "edkm_backward_buckets": ([P, i32, pp, P, i32, P, P, P], i32),
+            "edkm_backward_gamma": ([i32, pp, P, P, P, P, P], i32),
+            "edkm_backward_table": ([i32, pp, P, P, P, P, P, P], i32),
+            "edkm_backward_dw": ([P, i32, pp, P, i32, P, P, P, i32, P], i32),
             "edkm_read_status": ([P, i32, pp, P, P, P], i32),
             "edkm_last_launch_count": ([], i32),
             "edkm_status_string": ([i32], ctypes.c_char_p),
@@ -82,7 +86,8 @@ def lib():
 
 def exported_symbols() -> list:
     return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_forward", "edkm_reconstruct",
-            "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_read_status",
+            "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_backward_buckets",
+            "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
             "edkm_last_launch_count", "edkm_status_string", "edkm_last_error"]
 
 
@@ -301,6 +306,32 @@ class Plan:
                                           _ptr(self.saved), _ptr(self.ws), _ptr(self.gamma), _stream(stream)),
                "edkm_backward_reduce")
         return self.gamma
+
+    # the four backward kernels individually (B1, TGAMMA, TB, B2)
+    def backward_buckets(self, weights, grads, stream=None):
+        gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
+        _check(lib().edkm_backward_buckets(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
+                                           self._arr("g", grads, _ptr_array), gdt, _ptr(self.saved), _ptr(self.ws),
+                                           _stream(stream)), "edkm_backward_buckets")
+
+    def backward_gamma(self, stream=None):
+        _check(lib().edkm_backward_gamma(self.nt, ctypes.byref(self.p.c()), _ptr(self.counts), _ptr(self.saved),
+                                         _ptr(self.ws), _ptr(self.gamma), _stream(stream)), "edkm_backward_gamma")
+        return self.gamma
+
+    def backward_table(self, stream=None):
+        _check(lib().edkm_backward_table(self.nt, ctypes.byref(self.p.c()), _ptr(self.counts), _ptr(self.saved),
+                                         _ptr(self.ws), _ptr(self.gamma), _ptr(self.dC0), _stream(stream)),
+               "edkm_backward_table")
+        return self.dC0
+
+    def backward_dw(self, weights, grads, dW, stream=None):
+        gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
+        ddt = _DT[dW[0].dtype] if dW else _DT[self.p.wdtype]
+        _check(lib().edkm_backward_dw(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
+                                      self._arr("g", grads, _ptr_array), gdt, _ptr(self.saved), _ptr(self.ws),
+                                      self._arr("dw", dW, _ptr_array), ddt, _stream(stream)), "edkm_backward_dw")
+        return dW
 
     def backward_apply(self, weights, grads, dW, stream=None):
         gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
