@@ -30,8 +30,9 @@ namespace edkm {
 
 constexpr int kTThreads = 512;
 constexpr int kTWarps = kTThreads / 32;
-constexpr int kStage = 6144;  // rows per CTA staged in shared memory (v, n, psi: 24 B each)
-constexpr size_t kStageBytes = (size_t)kStage * 24;
+constexpr int kStage = 12288;  // rows per CTA staged in shared memory: value (f32), count (i32), psi (f64)
+constexpr size_t kStageBytesF = (size_t)kStage * 8;   // TF: value + count
+constexpr size_t kStageBytesB = (size_t)kStage * 16;  // TB: value + count + psi
 
 // Centroids of one iteration in the forms the attention needs: fp64 values, fp32 values
 // (to pick the nearest centroid), and per centroid pair (m, j) the fp64-derived difference
@@ -40,6 +41,8 @@ template <int K>
 struct CSet {
   double c[K];
   float hi[K];
+  float sv[K];   // fp32 centroids in ascending order (ties by index) ...
+  int sidx[K];   // ... and their indices: nearest-centroid search by bisection
   float dms[K][K];
   float ph[K][K], pl[K][K];
   // every thread of the block calls it; the caller synchronises before and after
@@ -53,9 +56,35 @@ struct CSet {
       pl[t / K][t % K] = (float)(p - (double)h);
     }
     if (t < K) {
-      c[t] = src[t];
-      hi[t] = (float)src[t];
+      const double ct = src[t];
+      c[t] = ct;
+      hi[t] = (float)ct;
+      int rank = 0;
+      for (int l = 0; l < K; ++l) rank += (src[l] < ct) || (src[l] == ct && l < t);
+      sv[rank] = (float)ct;
+      sidx[rank] = t;
     }
+  }
+  // index of a nearest centroid to v (ties either way: any near-minimum keeps the
+  // reduced logits in range; the attention itself is exact in the choice)
+  __device__ __forceinline__ int nearest(float vf) const {
+    if (K <= 4) {
+      int jm = 0;
+      float am = fabsf(vf - hi[0]);
+#pragma unroll
+      for (int j = 1; j < K; ++j) {
+        const float a = fabsf(vf - hi[j]);
+        if (a < am) { am = a; jm = j; }
+      }
+      return jm;
+    }
+    int pos = 0;
+#pragma unroll
+    for (int st = K / 2; st >= 1; st >>= 1)
+      if (sv[pos + st - 1] < vf) pos += st;
+    // candidates sv[pos-1], sv[pos]
+    const int lo = pos > 0 ? pos - 1 : 0;
+    return (fabsf(vf - sv[lo]) <= fabsf(vf - sv[pos])) ? sidx[lo] : sidx[pos];
   }
 };
 
@@ -75,13 +104,7 @@ __device__ __forceinline__ float ex2(float x) {
 // patterns is done by the callers in fp64 (R7).
 template <int K>
 __device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float (&A)[K]) {
-  int jm = 0;
-  float am = fabsf(vf - cs.hi[0]);
-#pragma unroll
-  for (int j = 1; j < K; ++j) {
-    const float a = fabsf(vf - cs.hi[j]);
-    if (a < am) { am = a; jm = j; }
-  }
+  const int jm = cs.nearest(vf);
   const float* dmr = cs.dms[jm];
   const float* phr = cs.ph[jm];
   const float* plr = cs.pl[jm];
@@ -127,24 +150,24 @@ __device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, d
   __syncthreads();
 }
 
-// Rows of one partition: patterns in rows[], values/counts staged in shared memory
-// for r < kStage, re-derived from global memory beyond (rare: U > kStage per CTA).
+// Rows of one partition: patterns in rows[]; value (exact in fp32), count and the running psi
+// staged in shared memory for r < kStage, read from global memory beyond (U > kStage per CTA).
 struct RowStage {
   const uint16_t* rows;
   const int32_t* cnt;
-  double* sv;    // [kStage] value v_u
-  double* sn;    // [kStage] count n_u
+  float* sv;     // [kStage] value v_u
+  int32_t* sn;   // [kStage] count n_u
   double* spsi;  // [kStage] psi accumulator (TB)
   double* gpsi;  // global psi for r >= kStage
   int nr, wdtype;
-  __device__ __forceinline__ double v(int r) const { return r < kStage ? sv[r] : decode16(rows[r], wdtype); }
-  __device__ __forceinline__ double n(int r) const { return r < kStage ? sn[r] : (double)cnt[rows[r]]; }
+  __device__ __forceinline__ double v(int r) const { return r < kStage ? (double)sv[r] : decode16(rows[r], wdtype); }
+  __device__ __forceinline__ double n(int r) const { return (double)(r < kStage ? sn[r] : cnt[rows[r]]); }
   __device__ __forceinline__ double& psi(int r) const { return r < kStage ? spsi[r] : gpsi[r]; }
   __device__ void stage() {
     for (int r = threadIdx.x; r < nr && r < kStage; r += blockDim.x) {
       const uint32_t u = rows[r];
-      sv[r] = decode16(u, wdtype);
-      sn[r] = (double)cnt[u];
+      sv[r] = decode16f(u, wdtype);
+      sn[r] = cnt[u];
     }
     __syncthreads();
   }
@@ -246,7 +269,8 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     st->nrows[crank] = nr;
     if (crank == 0) st->cl = cl;
   }
-  RowStage R{rows, cnt, stage_mem, stage_mem + kStage, stage_mem + 2 * kStage, nullptr, nr, P.wdtype};
+  RowStage R{rows, cnt, reinterpret_cast<float*>(stage_mem), reinterpret_cast<int32_t*>(stage_mem) + kStage, nullptr,
+             nullptr, nr, P.wdtype};
   R.stage();
 
   // ---- 2. unrolled centroid updates
@@ -389,8 +413,9 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
   // heuristic in TF) that is the single partition `crank`, staged in shared memory
   const bool one = pcl == cl;
   const int chunk = kPatterns / pcl;
-  RowStage R{P.rows + (int64_t)t * kPatterns + crank * chunk, cnt, stage_mem, stage_mem + kStage,
-             stage_mem + 2 * kStage, psi + crank * chunk, one ? st->nrows[crank] : 0, P.wdtype};
+  RowStage R{P.rows + (int64_t)t * kPatterns + crank * chunk, cnt, reinterpret_cast<float*>(stage_mem + kStage),
+             reinterpret_cast<int32_t*>(stage_mem + kStage) + kStage, stage_mem, psi + crank * chunk,
+             one ? st->nrows[crank] : 0, P.wdtype};
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
@@ -467,20 +492,36 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       const double ps = T > 0 ? (one ? R.psi(r) : gpsi[r]) : 0.0;
       pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
     }
-    // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN
-    for (int u = p * chunk + tid; u < (p + 1) * chunk; u += kTThreads)
-      if (!pattern_finite(u, P.wdtype) || cnt[u] == 0)
-        pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+    // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN.
+    // 16 patterns per thread per step (vector loads of the counts).
+    const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+    for (int u0 = p * chunk + tid * 16; u0 < (p + 1) * chunk; u0 += kTThreads * 16) {
+      const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
+      int c[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 x = __ldg(c4 + q);
+        c[4 * q] = x.x;
+        c[4 * q + 1] = x.y;
+        c[4 * q + 2] = x.z;
+        c[4 * q + 3] = x.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (!pattern_finite(u0 + e, P.wdtype) || c[e] == 0) pp[u0 + e] = nan2;
+    }
   }
   cluster.sync();
 }
 
 // ============================================================================ launchers
+// CTAs per tensor: fill the GPU for small nt; at least 2 (the positive and negative
+// pattern halves, which split a symmetric weight distribution evenly) so a CTA stages
+// at most 32K rows
 int table_cluster_size(int nt) {
   if (nt <= 18) return 8;
   if (nt <= 37) return 4;
-  if (nt <= 74) return 2;
-  return 1;
+  return 2;
 }
 
 template <class Fn>
@@ -516,8 +557,8 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
     }                                                       \
   }
 
-EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytes)
+EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytesF)
 EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0)
-EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytes)
+EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytesB)
 
 }  // namespace edkm
