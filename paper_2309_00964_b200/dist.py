@@ -44,16 +44,17 @@ class ShardedStep:
     B200 it is paper_2309_00964_b200.edkm.Plan.
     """
 
-    def __init__(self, kernels, group=None):
+    def __init__(self, kernels, group=None, allreduce=None):
         self.k = kernels
         self.group = group
+        self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
 
     def __call__(self, weights, grads, C0, outs, dW):
         self.k.uniquify(weights)
-        allreduce_sum(self.k.counts, self.group)          # exchange 1: integer counts
+        self.allreduce(self.k.counts)                     # exchange 1: integer counts
         self.k.forward(C0)
         self.k.reconstruct(weights, outs)
         self.k.backward_reduce(weights, grads)
-        allreduce_sum(self.k.gamma, self.group)           # exchange 2: gamma_T partials
+        self.allreduce(self.k.gamma)                      # exchange 2: gamma_T partials
         self.k.backward_apply(weights, grads, dW)
         return self.k.dC0

@@ -1,0 +1,99 @@
+"""The sharded N>1 path end to end on the CUDA kernels: two processes share the one B200,
+each holding a contiguous slice of every tensor, exchanging counts and gamma_T over
+a gloo process group (NCCL cannot put two ranks on one device; the exchanged tensors and the
+orchestration -- paper_2309_00964_b200.dist.ShardedStep driving edkm.Plan -- are the same).
+The concatenated slices of W~ and dW, and the rank-identical C_T and dC_0, must match the
+dense oracle on the whole tensors; counts after the all-reduce are bit-exact.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2309_00964_b200 import edkm as E
+from paper_2309_00964_b200 import synth
+from paper_2309_00964_b200.dist import ShardedStep, allreduce_sum, shard_all  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+SIZES = [200_003, 65_536 * 2 + 7, 50_000]
+P_ = dict(bits=3, tau=1e-3, max_iter=4)
+
+
+def _reduce_via_host(t: torch.Tensor):
+    h = t.cpu()
+    allreduce_sum(h)
+    t.copy_(h)
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        p = E.Params(torch.bfloat16, **P_)
+        Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
+        Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i) for i, n in enumerate(SIZES)]
+        rng = shard_all(SIZES, rank, world)
+        Wl = [w[a:b].contiguous().to(dev) for w, (a, b) in zip(Ws, rng)]
+        Gl = [g[a:b].contiguous().to(dev) for g, (a, b) in zip(Gs, rng)]
+        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
+        plan = E.Plan([w.numel() for w in Wl], p, dev)
+        outs = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
+        dW = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
+        ShardedStep(plan, allreduce=_reduce_via_host)(Wl, Gl, C0, outs, dW)
+        torch.cuda.synchronize()
+        q.put((rank, plan.counts.cpu().numpy(), plan.C_out.cpu().numpy(), plan.dC0.cpu().numpy(),
+               [o.cpu().double().numpy() for o in outs], [d.cpu().double().numpy() for d in dW]))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_two_ranks_on_one_gpu_match_single_process_oracle():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=600)
+        res[r[0]] = r
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
+    Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i) for i, n in enumerate(SIZES)]
+    k = 1 << P_["bits"]
+    C0 = np.float32(synth.quantile_centroids(k, 1.0)).astype(np.float64)
+    for t, n in enumerate(SIZES):
+        bits = Ws[t].view(torch.int16).numpy().view(np.uint16)
+        w = O.decode16(bits, O.BF16)
+        Ct, St, _ = O.dkm_forward(w, C0, P_["tau"], P_["max_iter"])
+        Wt = O.reconstruct(w, Ct[-1], P_["tau"])
+        dW, dC = O.dkm_backward(w, Gs[t].double().numpy(), Ct, St, P_["tau"])
+        for r in range(world):
+            assert np.array_equal(res[r][1][t], O.histogram(bits).astype(np.int32))  # global counts, exact
+            assert np.array_equal(res[r][2][t], res[0][2][t])                        # C_T rank-identical
+            assert np.array_equal(res[r][3][t], res[0][3][t])                        # dC_0 rank-identical
+        assert np.max(np.abs(res[0][2][t] - Ct[-1])) <= TOL * np.max(np.abs(Ct[-1]))
+        assert np.max(np.abs(res[0][3][t] - dC)) <= TOL * np.max(np.abs(dC))
+        gWt = np.concatenate([res[r][4][t] for r in range(world)])
+        gdW = np.concatenate([res[r][5][t] for r in range(world)])
+        assert np.max(np.abs(gWt - Wt)) <= TOL * np.max(np.abs(Wt))
+        assert np.max(np.abs(gdW - dW)) <= TOL * np.max(np.abs(dW))

@@ -43,6 +43,21 @@ __global__ void k_read8(const uint4* w, size_t n32, uint32_t* out) {
   }
   if (acc == 0x12345678u) out[0] = acc;
 }
+// copy with 256-bit loads/stores, U vectors in flight per thread
+template <int U>
+__global__ void k_copy8(const uint4* w, size_t n32, uint4* out) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n32; i += U * stride) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ldg_stream8(w + 2 * (i + u * stride), a[u], b[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(out + 2 * (i + u * stride)),
+                   "r"(a[u].x), "r"(a[u].y), "r"(a[u].z), "r"(a[u].w), "r"(b[u].x), "r"(b[u].y), "r"(b[u].z), "r"(b[u].w) : "memory");
+  }
+}
 __global__ void k_read(const uint4* w, size_t n16, uint32_t* out) {
   uint32_t acc = 0;
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -172,6 +187,11 @@ int main() {
   run("read_stream 148*4x512", [&] { k_read<<<sms * 4, 512>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("read_v8 148*4x512", [&] { k_read8<<<sms * 4, 512>>>((const uint4*)w, n16 / 2, o); }, n * 2.0);
   run("read_v8 148*8x256", [&] { k_read8<<<sms * 8, 256>>>((const uint4*)w, n16 / 2, o); }, n * 2.0);
+  run("copy v8 148x1024 U2", [&] { k_copy8<2><<<sms, 1024>>>((const uint4*)w, n16 / 2, out); }, n * 4.0);
+  run("copy v8 148x1024 U1", [&] { k_copy8<1><<<sms, 1024>>>((const uint4*)w, n16 / 2, out); }, n * 4.0);
+  run("copy v8 148*2x1024 U2", [&] { k_copy8<2><<<sms * 2, 1024>>>((const uint4*)w, n16 / 2, out); }, n * 4.0);
+  run("copy v8 148*4x512 U4", [&] { k_copy8<4><<<sms * 4, 512>>>((const uint4*)w, n16 / 2, out); }, n * 4.0);
+  run("copy v8 148*8x256 U2", [&] { k_copy8<2><<<sms * 8, 256>>>((const uint4*)w, n16 / 2, out); }, n * 4.0);
   cudaFuncSetAttribute(k_hist<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaFuncSetAttribute(k_hist<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaFuncSetAttribute(k_hist<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
