@@ -76,7 +76,7 @@ class OracleKernels:
 
 
 def inputs():
-    sizes = [10_007, 3, 65_536 + 17]
+    sizes = [10_007, 3, 1, 65_536 + 17]  # the 1-element tensor leaves rank 0 an empty slice
     Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 700 + i) for i, n in enumerate(sizes)]
     Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 800 + i) for i, n in enumerate(sizes)]
     C0 = torch.tensor([synth.quantile_centroids(K, 1.0)] * len(sizes), dtype=torch.float64)
@@ -150,5 +150,5 @@ def test_world_size_2_gloo_matches_single_process_oracle():
         assert np.max(np.abs(res[0][3][t] - dC)) <= 1e-10 * max(np.max(np.abs(dC)), 1e-300) + 1e-300
         got_Wt = np.concatenate([res[r][1][t] for r in range(world)])
         got_dW = np.concatenate([res[r][2][t] for r in range(world)])
-        np.testing.assert_allclose(got_Wt, Wt, rtol=1e-12, atol=1e-14)
+        assert np.max(np.abs(got_Wt - Wt)) <= 1e-10 * np.max(np.abs(Wt)), (t, np.max(np.abs(got_Wt - Wt)))
         assert np.max(np.abs(got_dW - dW)) <= 1e-10 * np.max(np.abs(dW))
