@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-groups", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -313,7 +314,7 @@ def main():
         torch.cuda.synchronize()
 
         from paper_2309_00964_b200.pipeline import HostPipeline
-        pipe = HostPipeline(numels, p, dev, n_groups=8, allreduce=allreduce if distributed else None,
+        pipe = HostPipeline(numels, p, dev, n_groups=args.e2e_groups, allreduce=allreduce if distributed else None,
                             buffers=(Ws, Gs, Wt, dW))
 
         def e2e_step():
@@ -336,7 +337,7 @@ def main():
         bytes_out = sum(w.numel() * 2 * 2 for w in Ws)
         e2e = {"value": n_total / (float(te.item()) / 1e3), "unit": "weights/s", "h2d_bytes_per_step": bytes_in,
                "d2h_bytes_per_step": bytes_out, "ms_per_step": float(te.item()), "steps": args.e2e_steps,
-               "path": "pipeline.HostPipeline (8 tensor groups; H2D, the C-ABI step and D2H overlap on 3 streams); pinned host W, G in and W~, dW out every step"}
+               "path": f"pipeline.HostPipeline ({args.e2e_groups} tensor groups; H2D, the C-ABI step and D2H overlap on 3 streams); pinned host W, G in and W~, dW out every step"}
         del hW, hG, hWt, hdW
 
     if rank != 0:
