@@ -88,7 +88,7 @@ __device__ __forceinline__ uint32_t pat(const V8& v, int e) { return (v.x[e >> 1
 
 // ============================================================================ F1
 struct F1Policy {
-  static constexpr int kLoop = 1;  // two vectors per iteration
+  static constexpr int kLoop = 1;  // two vectors per iteration (F1 is atomic-bound: more loads in flight)
   const StreamArgs& A;
   uint32_t* h;
   int32_t* counts;  // [nt_total][65536], this launch's tensors start at t0
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
 
 template <int MODE>
 struct F2Policy {
-  static constexpr int kLoop = 1;
+  static constexpr int kLoop = 0;  // one vector per iteration (measured faster for the gather)
   const StreamArgs& A;
   const F2Args& F;
   unsigned char* sm;
