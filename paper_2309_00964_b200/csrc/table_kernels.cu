@@ -28,8 +28,8 @@ namespace cg = cooperative_groups;
 
 namespace edkm {
 
-constexpr int kTThreads = 512;
-constexpr int kTWarps = kTThreads / 32;
+constexpr int kFThreads = 256;  // TF, TGAMMA: small shared footprint, two CTAs per SM
+constexpr int kBThreads = 512;  // TB: 192 KiB of staged rows, one CTA per SM
 constexpr int kStage = 12288;  // rows per CTA staged in shared memory: value (f32), count (i32), psi (f64)
 constexpr size_t kStageBytesF = (size_t)kStage * 8;   // TF: value + count
 constexpr size_t kStageBytesB = (size_t)kStage * 16;  // TB: value + count + psi
@@ -123,7 +123,7 @@ __device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float
 // Sum N doubles over the CTA then over the cluster; result in tot[0..N) of every CTA.
 // `part` is a [2][N] shared buffer used with alternating parity so one cluster
 // barrier per call suffices.
-template <int N>
+template <int N, int NW>
 __device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, double* part, double* tot, int parity,
                                                   cg::cluster_group& cluster) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -138,7 +138,7 @@ __device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, d
   double* mine = part + parity * N;
   if (threadIdx.x < N) {
     double s = 0.0;
-    for (int w = 0; w < kTWarps; ++w) s += red[w * N + threadIdx.x];
+    for (int w = 0; w < NW; ++w) s += red[w * N + threadIdx.x];
     mine[threadIdx.x] = s;
   }
   cluster.sync();
@@ -175,16 +175,16 @@ struct RowStage {
 
 // ============================================================================ TF
 template <int K>
-__global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
+__global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   __shared__ double sC[K], sCn[K], sCf[K], sDelta[K];
-  __shared__ double red[kTWarps * 2 * K], part[2 * 2 * K], tot[2 * K];
+  __shared__ double red[(kFThreads / 32) * 2 * K], part[2 * 2 * K], tot[2 * K];
   __shared__ CSet<K> cs;
-  __shared__ int s_scan[kTWarps];
-  __shared__ long long s_nf[kTWarps];
+  __shared__ int s_scan[(kFThreads / 32)];
+  __shared__ long long s_nf[(kFThreads / 32)];
 
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
   const int chunk = kPatterns / cl, base = crank * chunk;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   //         page masses (every present pattern), non-finite counts, NaN-fill of the W~ tables
   int nr = 0;
   long long nonfin = 0;
-  for (int off = 0; off < chunk; off += kTThreads * 16) {
+  for (int off = 0; off < chunk; off += kFThreads * 16) {
     const int u0 = base + off + tid * 16;
     int c[16];
     const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     if (lane == 31) s_scan[warp] = incl;
     __syncthreads();
     int woff = 0, btot = 0;
-    for (int w = 0; w < kTWarps; ++w) {
+    for (int w = 0; w < (kFThreads / 32); ++w) {
       const int x = s_scan[w];
       woff += (w < warp) ? x : 0;
       btot += x;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   __syncthreads();  // also orders the rows[] writes before staging
   if (tid == 0) {
     long long s = 0;
-    for (int w = 0; w < kTWarps; ++w) s += s_nf[w];
+    for (int w = 0; w < (kFThreads / 32); ++w) s += s_nf[w];
     st->nonfinite[crank] = s;
     st->nrows[crank] = nr;
     if (crank == 0) st->cl = cl;
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
     double acc[2 * K];
 #pragma unroll
     for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
-    for (int r = tid; r < nr; r += kTThreads) {
+    for (int r = tid; r < nr; r += kFThreads) {
       const double v = R.v(r), n = R.n(r), nv = n * v;
       float A[K];
       attention_row<K>((float)v, cs, A);
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
         acc[K + j] = fma((double)A[j], nv, acc[K + j]);
       }
     }
-    cluster_allreduce<2 * K>(acc, red, part, tot, it & 1, cluster);
+    cluster_allreduce<2 * K, kFThreads / 32>(acc, red, part, tot, it & 1, cluster);
     if (tid < K) {
       const double S = tot[tid], M = tot[K + tid];
       const double cn = (S != 0.0) ? M / S : sC[tid];
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
   __syncthreads();
 
   // ---- 3. per populated pattern: W~ (fp32 and 16-bit), hard index vs the fp32 C_out
-  for (int r = tid; r < nr; r += kTThreads) {
+  for (int r = tid; r < nr; r += kFThreads) {
     const uint32_t u = rows[r];
     const double v = R.v(r);
     int best = 0;
@@ -355,10 +355,10 @@ __global__ void __launch_bounds__(kTThreads) tf_kernel(const TableArgs P) {
 
 // ============================================================================ TGAMMA
 template <int K>
-__global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
+__global__ void __launch_bounds__(kFThreads) tgamma_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ double red[(kFThreads / 32) * K], part[2 * K], tot[K];
   __shared__ CSet<K> cs;
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
   for (int p = crank; p < pcl; p += cl) {
     const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * (kPatterns / pcl);
     const int nr = st->nrows[p];
-    for (int r = tid; r < nr; r += kTThreads) {
+    for (int r = tid; r < nr; r += kFThreads) {
       const uint32_t u = rows[r];
       const double B = Bt[u];
       if (B == 0.0) continue;
@@ -389,18 +389,18 @@ __global__ void __launch_bounds__(kTThreads) tgamma_kernel(const TableArgs P) {
       for (int l = 0; l < K; ++l) acc[l] += B * A[l] * (1.0 + (sC[l] - wt) * 2.0 * (v - sC[l]) * P.inv_tau);
     }
   }
-  cluster_allreduce<K>(acc, red, part, tot, 0, cluster);
+  cluster_allreduce<K, kFThreads / 32>(acc, red, part, tot, 0, cluster);
   if (crank == 0 && tid < K) P.gamma[(int64_t)t * K + tid] = tot[tid];
   cluster.sync();
 }
 
 // ============================================================================ TB
 template <int K>
-__global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
+__global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[kTWarps * K], part[2 * K], tot[K];
+  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
   __shared__ CSet<K> cs;
   const double* sCt = cs.c;
   const TensorState* st = P.state + t;
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
       const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
       double* gpsi = psi + p * chunk;
       const int nr = one ? R.nr : st->nrows[p];
-      for (int r = tid; r < nr; r += kTThreads) {
+      for (int r = tid; r < nr; r += kBThreads) {
         const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
         const double n = one ? R.n(r) : (double)cnt[rows[r]];
         float Af[K];
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
         ps = (it == T - 1 ? 0.0 : ps) + dpsi;
       }
     }
-    cluster_allreduce<K>(acc, red, part, tot, it & 1, cluster);
+    cluster_allreduce<K, kBThreads / 32>(acc, red, part, tot, it & 1, cluster);
     if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
     __syncthreads();
   }
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
     const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
     double* gpsi = psi + p * chunk;
     const int nr = one ? R.nr : st->nrows[p];
-    for (int r = tid; r < nr; r += kTThreads) {
+    for (int r = tid; r < nr; r += kBThreads) {
       const uint32_t u = rows[r];
       const double v = one ? R.v(r) : decode16(u, P.wdtype);
       float Af[K];
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kTThreads) tb_kernel(const TableArgs P) {
     // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN.
     // 16 patterns per thread per step (vector loads of the counts).
     const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
-    for (int u0 = p * chunk + tid * 16; u0 < (p + 1) * chunk; u0 += kTThreads * 16) {
+    for (int u0 = p * chunk + tid * 16; u0 < (p + 1) * chunk; u0 += kBThreads * 16) {
       const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
       int c[16];
 #pragma unroll
@@ -525,7 +525,7 @@ int table_cluster_size(int nt) {
 }
 
 template <class Fn>
-static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_t smem) {
+static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_t smem, int threads) {
   if (P.nt == 0) return cudaSuccess;
   if (smem) {
     cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -533,7 +533,7 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(P.nt * P.cl));
-  cfg.blockDim = dim3(kTThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -546,19 +546,19 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
   return cudaLaunchKernelEx(&cfg, fn, P);
 }
 
-#define EDKM_TABLE_LAUNCH(NAME, KERNEL, SMEM)             \
-  cudaError_t NAME(const TableArgs& P, cudaStream_t s) {    \
-    switch (P.k) {                                          \
-      case 2: return launch_table(P, s, KERNEL<2>, SMEM);   \
-      case 4: return launch_table(P, s, KERNEL<4>, SMEM);   \
-      case 8: return launch_table(P, s, KERNEL<8>, SMEM);   \
-      case 16: return launch_table(P, s, KERNEL<16>, SMEM); \
-      default: return cudaErrorInvalidValue;                \
-    }                                                       \
+#define EDKM_TABLE_LAUNCH(NAME, KERNEL, SMEM, NT)              \
+  cudaError_t NAME(const TableArgs& P, cudaStream_t s) {         \
+    switch (P.k) {                                               \
+      case 2: return launch_table(P, s, KERNEL<2>, SMEM, NT);    \
+      case 4: return launch_table(P, s, KERNEL<4>, SMEM, NT);    \
+      case 8: return launch_table(P, s, KERNEL<8>, SMEM, NT);    \
+      case 16: return launch_table(P, s, KERNEL<16>, SMEM, NT);  \
+      default: return cudaErrorInvalidValue;                     \
+    }                                                            \
   }
 
-EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytesF)
-EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0)
-EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytesB)
+EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytesF, kFThreads)
+EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
+EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytesB, kBThreads)
 
 }  // namespace edkm
