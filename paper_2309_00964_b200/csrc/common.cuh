@@ -243,6 +243,26 @@ __device__ __forceinline__ void fixed_add(uint32_t saddr, int q) {
       : "memory");
 }
 
+// The same add in two halves so a thread can have many lo atomics in flight before it looks
+// at any return value: fixed_lo issues lo += q, fixed_carry applies the carry/borrow.
+__device__ __forceinline__ uint32_t fixed_lo(uint32_t saddr, int q) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(q));
+  return old;
+}
+template <uint32_t HI_OFF>
+__device__ __forceinline__ void fixed_carry(uint32_t saddr, int q, uint32_t old) {
+  asm volatile(
+      "{\n\t.reg .pred c, n, f;\n\t.reg .u32 nw, d;\n\t"
+      "add.u32 nw, %1, %2;\n\t"
+      "setp.lt.u32 c, nw, %1;\n\t"
+      "setp.lt.s32 n, %2, 0;\n\t"
+      "xor.pred f, c, n;\n\t"
+      "selp.u32 d, 1, 0xFFFFFFFF, c;\n\t"
+      "@f red.shared.add.u32 [%0+%3], d;\n\t}"
+      ::"r"(saddr), "r"(old), "r"(q), "n"(HI_OFF));
+}
+
 // (phi, psi) of a pattern: shared window when `in` != 0, else the global table
 // entry gtab[u] (its address is formed inside the predicated block).
 __device__ __forceinline__ float2 lookup_f2(uint32_t in, uint32_t saddr, const float2* gtab, uint32_t u) {

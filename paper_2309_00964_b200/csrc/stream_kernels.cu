@@ -241,11 +241,25 @@ __global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_con
 // (predicated, correct, slower).  At the end of the segment the exact per-CTA
 // sums are converted to fp64 once and added to the global buckets.
 // GDT: gradient dtype (kBF16, kFP16, kFP32).
+#ifndef EDKM_B1_LOOP
+#define EDKM_B1_LOOP 0
+#endif
+#ifndef EDKM_B2_LOOP
+#define EDKM_B2_LOOP 0
+#endif
+#ifndef EDKM_B1_BATCH
+#define EDKM_B1_BATCH 8
+#endif
 template <int GDT>
 struct B1Policy {
-  static constexpr int kLoop = 0;
+  static constexpr int kLoop = EDKM_B1_LOOP;
   static constexpr int GF32 = GDT == kFP32;
   static constexpr uint32_t kHiOff = 2 * kB1Pages * 256 * 4;  // byte offset of hi[] from lo[]
+  // lo[] starts at 2^31 (the slot value is hi*2^32 + lo - 2^31): a zero-mean running sum then
+  // wraps lo only when it leaves (-2^31, 2^31), not at every sign change, so the carry/borrow
+  // atomic is rare instead of a second atomic for most warps.
+  static constexpr uint32_t kLoBias = 0x80000000u;
+  static constexpr int kB1Batch = EDKM_B1_BATCH;  // lo atomics in flight per thread
   const StreamArgs& A;
   const B1Args& Bq;
   uint32_t* lo;
@@ -274,7 +288,7 @@ struct B1Policy {
     pbase = s_w[0];
     np = s_w[1];
     uint4* z = reinterpret_cast<uint4*>(lo);
-    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) z[s] = make_uint4(0, 0, 0, 0);
+    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) z[s] = make_uint4(kLoBias, kLoBias, kLoBias, kLoBias);
     uint4* zh = reinterpret_cast<uint4*>(hi);
     for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) zh[s] = make_uint4(0, 0, 0, 0);
     // scale from the max finite |G| of a sample (whole segment if the sample is all zero)
@@ -368,10 +382,23 @@ struct B1Policy {
     }
     const bool ok = GF32 ? gmax < glim : (max(gmax & 0xFFFFu, gmax >> 16) < glim16);
     if (active && max(rmax2 & 0xFFFFu, rmax2 >> 16) < win.np256 && ok) {
+      // all 16 lo atomics in flight first, then the (rare) carries: the return latency of
+      // one atomic is not paid per element
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
-        fixed_add<kHiOff>(win.baseP + slot * 4, __float2int_rn(g_of(r, e) * scale));
+      for (int h = 0; h < 16; h += kB1Batch) {
+        uint32_t old[kB1Batch];
+        int qv[kB1Batch];
+#pragma unroll
+        for (int e = h; e < h + kB1Batch; ++e) {
+          const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
+          qv[e - h] = __float2int_rn(g_of(r, e) * scale);
+          old[e - h] = fixed_lo(win.baseP + slot * 4, qv[e - h]);
+        }
+#pragma unroll
+        for (int e = h; e < h + kB1Batch; ++e) {
+          const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
+          fixed_carry<kHiOff>(win.baseP + slot * 4, qv[e - h], old[e - h]);
+        }
       }
     } else {
       // rare: re-read the 16 elements (dynamic indexing of the register vector would spill it)
@@ -385,7 +412,7 @@ struct B1Policy {
     if (active) {
       double* Bt = bucket(t);
       for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) {
-        const int64_t v = ((int64_t)hi[s] << 32) + (int64_t)lo[s];
+        const int64_t v = ((int64_t)hi[s] << 32) + (int64_t)lo[s] - (int64_t)kLoBias;
         if (v != 0) atomicAdd(&Bt[slot_pattern(s, pbase, np)], (double)v * inv_scale);
       }
     }
@@ -406,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) b1_bucket_kernel(const __grid_con
 // GDT: gradient dtype, ODT: dW dtype (kBF16, kFP16, kFP32).
 template <int GDT, int ODT>
 struct B2Policy {
-  static constexpr int kLoop = 0;
+  static constexpr int kLoop = EDKM_B2_LOOP;
   static constexpr int GF32 = GDT == kFP32, OF32 = ODT == kFP32;
   const StreamArgs& A;
   const B2Args& Bq;

@@ -24,7 +24,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libedkm.so")
+# EDKM_LIB selects another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("EDKM_LIB") or os.path.join(_HERE, "libedkm.so")
 
 BF16, FP16, FP32, U8 = 0, 1, 2, 3
 SOFT, HARD_VALUE, HARD_INDEX = 0, 1, 2
