@@ -113,7 +113,7 @@ def main():
         lines += ["", f"sum of kernel times: {tot/1e6:.3f} ms", ""]
     if a.full:
         f = full(a.full)
-        lines += ["## `--set full` (one launch each, tools/profile_step.py --workload cfg3)", "",
+        lines += ["## `--set full` (one launch of each kernel of one CFG3 step: tools/round_profile.sh)", "",
                   "| kernel | time (us) | DRAM GB | DRAM B/weight | SM clk GHz | inst/weight | issue active | warps active | L1tex/SMEM pipe | regs | grid x block |",
                   "|---|---|---|---|---|---|---|---|---|---|---|"]
         for k, d in f.items():
