@@ -1,7 +1,8 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
-CFG3 (full LLaMA-7B: 226 tensors, 6,738,149,376 bf16 weights, k=8, tau=1e-5, T=5) and CFG2
-(one decoder layer) run through one edkm.Plan exactly as bench.py does (bf16 W~ and dW).
+CFG3 (full LLaMA-7B: 226 tensors, 6,738,149,376 bf16 weights, k=8, tau=1e-5, T=5), CFG2
+(one decoder layer), CFG4 (the CFG3 shapes in fp16, k=16 and k=4, T=30) and CFG5 (LLaMA-13B,
+282 tensors) run through one edkm.Plan exactly as bench.py does (16-bit W~ and dW).
 Checked against the oracle on sampled tensors, in the attention-table form that
 tests/test_oracle.py pins to the dense definition: exact counts (bit-exact), C_T,
 the W~ table of every populated pattern, dC_0, and 200,000 sampled elements of W~ and dW
@@ -20,9 +21,11 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-def ulp_bf16(x):
-    t = torch.from_numpy(np.abs(x)).to(torch.bfloat16).to(torch.float64).numpy()
-    return np.maximum(2.0 ** (np.floor(np.log2(np.maximum(t, 1e-300))) - 7), 2.0 ** -133)
+def ulp16(x, dtype):
+    """One unit in the last place of the 16-bit output format at |x| (the rounding of W~ / dW)."""
+    mant, tiny = (7, 2.0 ** -133) if dtype == torch.bfloat16 else (10, 2.0 ** -24)
+    t = torch.from_numpy(np.abs(x)).to(dtype).to(torch.float64).numpy()
+    return np.maximum(2.0 ** (np.floor(np.log2(np.maximum(t, 1e-300))) - mant), tiny)
 
 
 def run(name, sample):
@@ -48,7 +51,7 @@ def run(name, sample):
         c = O.histogram(bits)
         assert np.array_equal(counts[t], c.astype(np.int32)), wl.shapes[t][0]
         u = np.nonzero(c)[0]
-        v = O.decode16(u.astype(np.uint16), O.BF16)
+        v = O.decode16(u.astype(np.uint16), O.BF16 if wl.wdtype == torch.bfloat16 else O.FP16)
         C0t = np.float32(C0[t].cpu().numpy()).astype(np.float64)
         Ct, St, _ = O.dkm_forward(v, C0t, wl.tau, wl.max_iter, mult=c[u])
         assert np.min(St) >= 1e-6 * bits.size
@@ -66,11 +69,11 @@ def run(name, sample):
         idx = rng.integers(0, bits.size, 200_000)
         wt_ref = tab[pos[idx]]
         wt_gpu = Wt[t].view(-1)[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-        assert np.all(np.abs(wt_gpu - wt_ref) <= ulp_bf16(wt_ref))
+        assert np.all(np.abs(wt_gpu - wt_ref) <= ulp16(wt_ref, wl.wdtype))
         dw_all = G * phi[pos] + psi[pos]
         dw_ref = dw_all[idx]
         dw_gpu = dW[t].view(-1)[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-        assert np.all(np.abs(dw_gpu - dw_ref) <= ulp_bf16(dw_ref) + TOL * np.max(np.abs(dw_all)))
+        assert np.all(np.abs(dw_gpu - dw_ref) <= ulp16(dw_ref, wl.wdtype) + TOL * np.max(np.abs(dw_all)))
 
 
 def test_cfg2_decoder_layer_all_tensors():
@@ -84,3 +87,20 @@ def test_cfg3_llama7b_sampled_tensors():
     sample = [0, names.index("layers.0.q_proj"), names.index("layers.17.gate_proj"),
               names.index("layers.31.down_proj"), len(names) - 1]
     run("cfg3", sample=sample)
+
+
+def _sample(name):
+    names = [s[0] for s in synth.workload(name).shapes]
+    return [0, names.index("layers.0.q_proj"), names.index("layers.17.gate_proj"),
+            names.index("layers.31.down_proj"), len(names) - 1]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg4", "cfg4_b2"])
+def test_cfg4_fp16_sweep_sampled_tensors(name):
+    run(name, sample=_sample(name))
+
+
+@pytest.mark.slow
+def test_cfg5_llama13b_sampled_tensors():
+    run("cfg5", sample=_sample("cfg5"))
