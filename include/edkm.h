@@ -158,6 +158,12 @@ edkm_status edkm_backward(const edkm_tensor* tensors, int nt, const edkm_params*
 edkm_status edkm_read_status(const void* saved, int nt, const edkm_params* p, int64_t* nonfinite_host,
                              int32_t* iters_host, void* stream);
 
+/* Caps the grid of the per-weight streaming kernels (F1, F2, B1, B2; one 1024-thread CTA per
+ * SM) launched by later calls on the calling thread at `ctas` CTAs, so that two calls on
+ * different streams can run side by side on disjoint SMs; ctas <= 0 restores the default
+ * (the SM count).  Results do not depend on it.  Returns the previous cap (0 = none). */
+int edkm_set_max_ctas(int ctas);
+
 /* Number of kernels the last successful entry point launched on the calling thread. */
 int edkm_last_launch_count(void);
 const char* edkm_status_string(int status);

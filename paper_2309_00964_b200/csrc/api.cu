@@ -16,6 +16,7 @@ namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
+thread_local int g_max_ctas = 0;  // edkm_set_max_ctas: cap on the streaming kernels' grid (0 = SM count)
 
 edkm_status fail(edkm_status st, const char* fmt, const char* detail = "") {
   snprintf(g_err, sizeof(g_err), fmt, detail);
@@ -31,7 +32,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
+  return g_max_ctas > 0 && g_max_ctas < n ? g_max_ctas : n;
 }
 
 bool params_ok(const edkm_params* p) {
@@ -414,6 +415,12 @@ edkm_status edkm_read_status(const void* saved, int nt, const edkm_params* p, in
 }
 
 int edkm_last_launch_count(void) { return g_launches; }
+
+int edkm_set_max_ctas(int ctas) {
+  const int prev = g_max_ctas;
+  g_max_ctas = ctas > 0 ? ctas : 0;
+  return prev;
+}
 
 const char* edkm_status_string(int status) {
   switch (status) {

@@ -121,10 +121,193 @@ struct F1Policy {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_constant__ StreamArgs A, int32_t* counts) {
+// ---------------------------------------------------------------------------- F1, lane-private
+// One shared counter array makes F1 bound by shared-memory bank conflicts, not HBM: the 32
+// random patterns of a warp's atomic land on the 32 banks like balls in bins (~3.8 wavefronts
+// per instruction, S4).  Here every lane owns a private copy of the counters that
+// lies entirely in its own bank (word = row * 32 + lane), so a warp's 32 atomics always hit 32
+// distinct banks: one wavefront per instruction.  32 copies fit for a window of kF1LPages
+// magnitude pages: word `row` = rel of a pattern (u & 0x7FFF) - pbase*256 holds the 16-bit
+// counters of both signs (positive in the low half).  A copy is shared by the 32 threads with
+// the same lane id, so after 32 x kF1LChunkVec x 16 < 65536 increments the copies are folded
+// into per-thread 32-bit accumulators (each thread owns rows tid and tid + 1024) and zeroed.
+// The window is chosen per segment from a sample; bf16 N(0, 0.02^2) keeps ~99.9% of the weights
+// in it (patterns outside go to global atomics).  A segment whose sample is not covered well
+// (fp16, whose pages are quarter binades, or unusual data) takes the shared-array path.
+constexpr int kF1LPages = 7;
+constexpr int kF1LRows = kF1LPages * 256;  // 1792 words per copy, 32 copies = 224 KiB
+constexpr int kF1LChunkVec = 127;          // vectors per thread between folds (32*127*16 < 65536)
+constexpr int kF1Sample = 16384;
+
+__device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u) { atomicAdd(&c[u], 1); }
+
+// fold the 32 copies of rows tid and tid+1024 into acc (pos, neg per row) and zero them
+__device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int r = tid + j * 1024;
+    if (r < kF1LRows) {
+      uint4* row = reinterpret_cast<uint4*>(h + r * 32);
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int q = (tid + s) & 7;  // diagonal: the 8 threads of a quarter warp read 8 distinct bank groups
+        const uint4 x = row[q];
+        lo += (x.x & 0xFFFFu) + (x.y & 0xFFFFu) + (x.z & 0xFFFFu) + (x.w & 0xFFFFu);
+        hi += (x.x >> 16) + (x.y >> 16) + (x.z >> 16) + (x.w >> 16);
+        row[q] = make_uint4(0, 0, 0, 0);
+      }
+      acc[2 * j] += lo;
+      acc[2 * j + 1] += hi;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_constant__ StreamArgs A, int32_t* counts,
+                                                              uint32_t k16, uint32_t k128) {
   extern __shared__ __align__(16) uint32_t smem_u32[];
-  F1Policy p{A, smem_u32, counts};
-  for_each_segment(A, p);
+  __shared__ uint32_t s_pg[kMagPages];
+  __shared__ int s_base, s_lp;
+  uint32_t* h = smem_u32;
+  int64_t lo, hi;
+  cta_range(A.total, lo, hi);
+  if (lo >= hi) return;
+  int t = find_tensor(A, lo);
+  const int tid = threadIdx.x, bs = blockDim.x, lane = tid & 31;
+  F1Policy gen{A, h, counts};
+  while (lo < hi) {
+    while (A.offs[t + 1] <= lo) ++t;
+    const int64_t a = lo - A.offs[t], b = min(hi, A.offs[t + 1]) - A.offs[t];
+    const uint16_t* w = A.w[t];
+    int32_t* cnt = counts + (int64_t)(A.t0 + t) * kPatterns;
+    // ---- choose the lane-private window from a sample of the segment
+    if (tid < kMagPages) s_pg[tid] = 0;
+    __syncthreads();
+    const int64_t se = min(b, a + kF1Sample);
+    if (A.wdtype == kBF16)
+      for (int64_t i = a + tid; i < se; i += bs) atomicAdd(&s_pg[(w[i] >> 8) & 0x7F], 1u);
+    __syncthreads();
+    if (tid == 0) {
+      // the kF1LPages consecutive magnitude pages holding most of the sample
+      uint32_t tot = 0, cur = 0, best = 0, bb = 0;
+      for (int p = 0; p < kMagPages; ++p) tot += s_pg[p];
+      for (int p = 0; p < kF1LPages; ++p) cur += s_pg[p];
+      best = cur;
+      for (int p = kF1LPages; p < kMagPages; ++p) {
+        cur += s_pg[p] - s_pg[p - kF1LPages];
+        if (cur > best) { best = cur; bb = p - kF1LPages + 1; }
+      }
+      s_base = (int)bb;
+      // lane-private path when the window holds >= 98% of a non-trivial sample
+      s_lp = A.wdtype == kBF16 && tot >= 1024 && (uint64_t)best * 50 >= (uint64_t)tot * 49;
+    }
+    __syncthreads();
+    if (s_lp) {
+      const uint32_t pb2 = ((0x10000u - ((uint32_t)s_base << 8)) & 0xFFFFu) * 0x10001u;  // -pbase*256, both halves
+      const uint32_t base = smem_addr(h) + (uint32_t)lane * 4u;
+      {
+        uint4* z = reinterpret_cast<uint4*>(h);
+        for (int i = tid; i < kF1LRows * 32 / 4; i += bs) z[i] = make_uint4(0, 0, 0, 0);
+      }
+      __syncthreads();
+      uint32_t acc[4] = {0, 0, 0, 0};
+      const uintptr_t wa = (uintptr_t)(w + a);
+      const int64_t head = min((int64_t)(((32u - (uint32_t)(wa & 31u)) & 31u) >> 1), b - a);
+      const int64_t va = a + head;
+      const int64_t nv = (b - va) >> 4;
+      for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global(cnt, w[i]);
+      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global(cnt, w[i]);
+      for (int64_t c0 = 0; c0 < nv; c0 += (int64_t)kF1LChunkVec * bs) {
+        const int64_t c1 = min(nv, c0 + (int64_t)kF1LChunkVec * bs);
+#pragma unroll 1
+        for (int64_t v = c0 + tid; v < c1; v += 2 * bs) {
+          V8 r[2];
+          const bool two = v + bs < c1;
+          r[0] = ldg_stream8(w + va + 16 * v);
+          if (two) r[1] = ldg_stream8(w + va + 16 * (v + bs));
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (k == 1 && !two) break;
+            uint32_t rel[8], rmax2 = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              rel[q] = __vadd2(r[k].x[q] & 0x7FFF7FFFu, pb2);
+              rmax2 = __vmaxu2(rmax2, rel[q]);
+            }
+            if (max(rmax2 & 0xFFFFu, rmax2 >> 16) < (uint32_t)kF1LRows) {
+              // Per 16-bit pair: row offsets by IMAD (k16, k128 are kernel parameters, opaque to
+              // ptxas, so the multiplies stay on the FMA pipe); the increment 1 or 0x10000 (sign of
+              // the pattern selects the counter half) from one PRMT sign-replicate + 1.  F1 is
+              // ALU-pipe bound otherwise (ncu: ALU 83%, FMA-heavy 34%).
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint32_t x = r[k].x[q];
+                const uint32_t rh = __umulhi(rel[q], k16);
+                const uint32_t rl = rel[q] & 0xFFFFu;
+                uint32_t mlo, mhi;
+                asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));  // 0xFFFF if bit 15 set
+                asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));  // 0xFFFF if bit 31 set
+                red_add_shared(rl * k128 + base, mlo + 1u);
+                red_add_shared(rh * k128 + base, mhi + 1u);
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint32_t x = r[k].x[q];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const uint32_t rr = e ? (rel[q] >> 16) : (rel[q] & 0xFFFFu);
+                  const uint32_t u = e ? (x >> 16) : (x & 0xFFFFu);
+                  if (rr < (uint32_t)kF1LRows) red_add_shared(base + (rr << 7), 1u + (u >> 15) * 0xFFFFu);
+                  else f1_count_global(cnt, u);
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        f1l_fold(h, acc);
+        __syncthreads();
+      }
+      // global counts of the window patterns: row r is rel, low half positive, high half negative
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = tid + j * 1024;
+        if (r < kF1LRows) {
+          const uint32_t u = ((uint32_t)s_base << 8) + (uint32_t)r;
+          if (acc[2 * j]) atomicAdd(&cnt[u], (int32_t)acc[2 * j]);
+          if (acc[2 * j + 1]) atomicAdd(&cnt[u | 0x8000u], (int32_t)acc[2 * j + 1]);
+        }
+      }
+      __syncthreads();
+    } else {
+      // shared-array path (the generic visitor's body for this one segment)
+      gen.begin(t, a, b);
+      const uintptr_t wa = (uintptr_t)(w + a);
+      const int64_t head = min((int64_t)(((32u - (uint32_t)(wa & 31u)) & 31u) >> 1), b - a);
+      const int64_t va = a + head;
+      const int64_t nv = (b - va) >> 4;
+      for (int64_t i = a + tid; i < a + head; i += bs) gen.scalar(t, i);
+      int64_t v = tid;
+      for (; v + bs < nv; v += 2 * bs) {
+        F1Policy::Vec r0, r1;
+        gen.load(t, va + 16 * v, r0);
+        gen.load(t, va + 16 * (v + bs), r1);
+        gen.process(t, va + 16 * v, r0);
+        gen.process(t, va + 16 * (v + bs), r1);
+      }
+      if (v < nv) {
+        F1Policy::Vec r0;
+        gen.load(t, va + 16 * v, r0);
+        gen.process(t, va + 16 * v, r0);
+      }
+      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) gen.scalar(t, i);
+      gen.end(t);
+    }
+    lo = A.offs[t] + b;
+    ++t;
+  }
 }
 
 // ============================================================================ F2
@@ -567,7 +750,7 @@ cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_
   const size_t smem = kF1Bins * sizeof(uint32_t);
   cudaError_t e = set_smem((const void*)f1_hist_kernel, smem);
   if (e != cudaSuccess) return e;
-  f1_hist_kernel<<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts);
+  f1_hist_kernel<<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, 0x10000u, 128u);
   return cudaGetLastError();
 }
 

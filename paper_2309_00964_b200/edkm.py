@@ -75,6 +75,7 @@ def lib():
             "edkm_backward_dw": ([P, i32, pp, P, i32, P, P, P, i32, P], i32),
             "edkm_read_status": ([P, i32, pp, P, P, P], i32),
             "edkm_last_launch_count": ([], i32),
+            "edkm_set_max_ctas": ([i32], i32),
             "edkm_status_string": ([i32], ctypes.c_char_p),
             "edkm_last_error": ([], ctypes.c_char_p),
         }
@@ -89,7 +90,7 @@ def exported_symbols() -> list:
     return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_forward", "edkm_reconstruct",
             "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_backward_buckets",
             "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
-            "edkm_last_launch_count", "edkm_status_string", "edkm_last_error"]
+            "edkm_last_launch_count", "edkm_set_max_ctas", "edkm_status_string", "edkm_last_error"]
 
 
 def _check(rc: int, what: str):
@@ -100,6 +101,11 @@ def _check(rc: int, what: str):
 
 def last_launch_count() -> int:
     return lib().edkm_last_launch_count()
+
+
+def set_max_ctas(ctas: int) -> int:
+    """Cap the streaming kernels' grid for later calls on this thread (0 = SM count); returns the old cap."""
+    return lib().edkm_set_max_ctas(int(ctas))
 
 
 @dataclass(frozen=True)

@@ -148,6 +148,52 @@ __global__ void __launch_bounds__(1024, 1) k_hist_l2(const uint4* w, size_t n16,
   if (s == 0x12345678u) gout[0] = s;
 }
 
+// lane-private replicas: 32 copies of packed u16 counters for NP magnitude pages x 2 signs, copy l
+// entirely in bank l (word = (slot >> 1) * 32 + lane), so a warp's 32 atomics never share a bank.
+// Patterns outside the window go to a shared u32 array (conflicting banks; ~0.5% of N(0,0.02^2)).
+// Timing only: the u16 counters are not flushed (the real kernel flushes every 2M elements).
+template <int NP, int V8>
+__global__ void __launch_bounds__(1024, 1) k_hist_lane(const uint4* w, size_t n16, uint32_t* gout, int pbase) {
+  extern __shared__ uint32_t h[];
+  constexpr int kWords = NP * 256 * 32;  // 2*NP*256 slots / 2 per word * 32 copies
+  constexpr int kLow = (232448 / 4 - kWords) & ~255;
+  uint32_t* lowc = h + kWords;
+  for (int i = threadIdx.x; i < kWords + kLow; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(h) + lane * 4u;
+  const uint32_t pb = (uint32_t)pbase * 256u, np256 = NP * 256u;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16 / (V8 ? 2 : 1); i += stride) {
+    uint32_t wd[8];
+    if (V8) {
+      uint4 a, b; ldg_stream8(w + 2 * i, a, b);
+      wd[0] = a.x; wd[1] = a.y; wd[2] = a.z; wd[3] = a.w; wd[4] = b.x; wd[5] = b.y; wd[6] = b.z; wd[7] = b.w;
+    } else {
+      uint4 v = ldg_stream(w + i);
+      wd[0] = v.x; wd[1] = v.y; wd[2] = v.z; wd[3] = v.w;
+    }
+#pragma unroll
+    for (int q = 0; q < (V8 ? 8 : 4); ++q) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t u = (wd[q] >> (16 * hh)) & 0xFFFFu;
+        const uint32_t rel = (u & 0x7FFFu) - pb;
+        if (rel < np256) {
+          const uint32_t slot = (u >> 15) * np256 + rel;
+          asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(base + (slot >> 1) * 128u), "r"(1u << ((slot & 1u) * 16u)));
+        } else {
+          asm volatile("red.shared.add.u32 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&lowc[u % (uint32_t)kLow])));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t s = 0;
+  for (int i = threadIdx.x; i < kWords + kLow; i += blockDim.x) s += h[i];
+  if (s == 0x12345678u) gout[0] = s;
+}
+
 // gather: out[i] = table[u_i] with a 128 KB bf16 table in SMEM
 __global__ void __launch_bounds__(1024, 1) k_gather(const uint4* w, size_t n16, uint4* out, const uint16_t* gtable) {
   extern __shared__ uint16_t t[];
@@ -224,6 +270,12 @@ int main() {
   run("hist u32 32K red", [&] { k_hist<2><<<sms, 1024, 131072>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom", [&] { k_hist<3><<<sms, 1024, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
   run("bucket f32 16K atom 3x/SM", [&] { k_hist<3><<<sms * 3, 1024 / 2, 65536>>>((const uint4*)w, n16, o); }, n * 2.0);
+  cudaFuncSetAttribute(k_hist_lane<6, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaFuncSetAttribute(k_hist_lane<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaFuncSetAttribute(k_hist_lane<7, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  run("hist lane-private 6pg v4", [&] { k_hist_lane<6, 0><<<sms, 1024, 232448>>>((const uint4*)w, n16, o, 57); }, n * 2.0);
+  run("hist lane-private 6pg v8", [&] { k_hist_lane<6, 1><<<sms, 1024, 232448>>>((const uint4*)w, n16, o, 57); }, n * 2.0);
+  run("hist lane-private 7pg v8", [&] { k_hist_lane<7, 1><<<sms, 1024, 232448>>>((const uint4*)w, n16, o, 56); }, n * 2.0);
   run("gather bf16 128K smem", [&] { k_gather<<<sms, 1024, 131072>>>((const uint4*)w, n16, out, tab); }, n * 4.0);
   return 0;
 }
