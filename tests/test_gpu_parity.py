@@ -264,6 +264,35 @@ def test_uniquify_edge_cases(case):
     assert np.array_equal(counts.cpu().numpy()[0], O.histogram(b).astype(np.int32))
 
 
+@pytest.mark.parametrize("ctas", [1, 3])
+@pytest.mark.parametrize("case", ["const_pos", "const_neg", "normal_plus_outliers", "two_signs_one_row"])
+def test_uniquify_lane_private_folds(case, ctas):
+    """F1's lane-private path: segments of several 2M-element chunks per CTA (folds of the 16-bit
+    copies at their limit, 32 x 127 x 16 = 65024 increments of one counter), both counter halves,
+    and patterns outside the sampled window (global atomics) -- bit-exact."""
+    n = 5_000_003
+    rng = np.random.default_rng(11)
+    if case == "const_pos":
+        b = np.full(n, 0x3F80, np.uint16)
+    elif case == "const_neg":
+        b = np.full(n, 0xBF80, np.uint16)
+    elif case == "two_signs_one_row":
+        b = np.where(rng.random(n) < 0.5, 0x3C12, 0xBC12).astype(np.uint16)
+    else:
+        w = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        b = (w.view(np.uint32) >> 16).astype(np.uint16)  # truncation: any bf16 pattern law will do
+        idx = rng.integers(0, n, 5000)
+        b[idx] = rng.choice(np.array([0x0000, 0x8000, 0x0001, 0x7F80, 0xFFC1, 0x7000, 0x1234], np.uint16), idx.size)
+    W = torch.from_numpy(b.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    old = E.set_max_ctas(ctas)
+    try:
+        counts = E.uniquify([W], E.Params(torch.bfloat16))
+        torch.cuda.synchronize()
+    finally:
+        E.set_max_ctas(old)
+    assert np.array_equal(counts.cpu().numpy()[0], O.histogram(b).astype(np.int32))
+
+
 def test_nonfinite_patterns_flagged_and_excluded():
     n = 100_000
     W = synth.normal_tensor(n, 1.0, torch.bfloat16, 21)
