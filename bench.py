@@ -248,15 +248,42 @@ def main():
         if distributed:
             dist.all_reduce(t)
 
+    # N > 1: exchange 1 fused into F1 over NVLS (dist.NvlsCounts) when the system supports it and
+    # it passes a bit-exact self-check against F1 + NCCL all-reduce; otherwise NCCL.
+    nv, exchange = None, "nccl all-reduce (counts int32, gamma fp64)"
+    mode = os.environ.get("EDKM_NVLS", "1")
+    if (world > 1 and mode != "0") or mode == "emulate":  # emulate: the protocol on plain memory, one rank
+        from paper_2309_00964_b200.dist import NvlsCounts
+        try:
+            nv = NvlsCounts(len(Ws), dev, emulate=mode == "emulate")
+            got = plan.uniquify_nvls(Ws, nv).clone()
+            want = E.uniquify(Ws, p)
+            allreduce(want)
+            ok = torch.tensor([float(torch.equal(got, want))], device=dev)
+            if distributed:
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() != 1.0:
+                raise RuntimeError("NVLS counts differ from the NCCL all-reduce")
+            exchange = "counts: NVLS multimem reductions fused into F1 + in-kernel arrival barrier; gamma: nccl all-reduce"
+        except Exception as e:  # no multicast, or a failed self-check: NCCL
+            if rank == 0:
+                print(f"bench: NVLS count exchange unavailable ({e}); using NCCL", file=sys.stderr)
+            nv = None
+            plan.counts = torch.empty((plan.nt, E.PATTERNS), dtype=torch.int32, device=dev)
+
     def step(ev=None):
         # the seven kernels of the hot path, one C-ABI call each, events between them
         def mark(i):
             if ev is not None:
                 ev[i].record(stream)
         mark(0)
-        plan.uniquify(Ws)                    # F1
-        mark(1)
-        allreduce(plan.counts)               # exchange 1 (N > 1)
+        if nv is not None:
+            plan.uniquify_nvls(Ws, nv)       # F1 + exchange 1 in the NVSwitch (N > 1)
+            mark(1)
+        else:
+            plan.uniquify(Ws)                # F1
+            mark(1)
+            allreduce(plan.counts)           # exchange 1 (N > 1)
         mark(2)
         plan.forward(C0)                     # TF
         mark(3)
@@ -298,7 +325,7 @@ def main():
     if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    launches_per_step = 7
+    launches_per_step = 7 + (nv is not None)  # + the NVLS arrival-barrier kernel
 
     # ---- end to end through the public API with host buffers (H2D of W, G; D2H of W~, dW every step)
     e2e = None
@@ -365,7 +392,7 @@ def main():
                                f"{'bf16' if wl.wdtype == torch.bfloat16 else 'fp16'} N(0,{wl.sigma}^2), "
                                f"b={wl.bits} (k={wl.k}), tau={wl.tau}, T={wl.max_iter}",
                    "tensors": len(wl.shapes), "weights": n_total, "bits": wl.bits, "tau": wl.tau,
-                   "iters": wl.max_iter, "parallelism": f"slices{world}",
+                   "iters": wl.max_iter, "parallelism": f"slices{world}", "exchange": exchange,
                    "arith": "bf16 I/O; fp32 per-weight passes; fp64 table phase",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
         "phases_ms": phase, "gpu_launches": launches_per_step * args.steps,

@@ -18,7 +18,8 @@
  *
  * Conventions for every entry point:
  *   - Device pointers unless stated.  The caller owns every buffer; the library
- *     allocates no device memory and keeps no state between calls.
+ *     allocates no device memory (except the edkm_mc_* NVLS buffers, on request) and
+ *     keeps no state between calls.
  *   - Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
  *     default stream).  No call synchronises the host except edkm_read_status.
  *   - Argument errors (null pointers with n > 0, bad dtype, bits outside 1..8,
@@ -86,6 +87,61 @@ size_t edkm_workspace_bytes(int nt, const edkm_params* p);
  * Exact (integer).  With several ranks the caller sums counts over ranks
  * (integer all-reduce) before edkm_forward. */
 edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, void* stream);
+
+/* F1 fused with the cross-rank sum of the counts over NVLink SHARP (NVLS) -- the in-kernel
+ * form of the integer all-reduce after edkm_uniquify (P:79 learners).
+ * Every buffer below is one symmetric allocation mapped on all ranks (e.g. torch symmetric
+ * memory); `*_mc` are its multicast addresses: a reduction issued there is applied by the
+ * NVSwitch to every rank's copy.
+ *   counts_mc : multicast address of an int32 [nt][65536] buffer that is ZERO on every rank
+ *               before any rank makes this call (callers alternate two buffers and zero the
+ *               one of the next step before this call, so a fast rank cannot add into a copy
+ *               that a slow rank has yet to clear).
+ *   flags_mc / flags : multicast / local address of EDKM_NVLS_FLAGS uint32 arrival counters,
+ *               zero-initialised once; never reset (monotonic).
+ *   epoch     : this rank's device step counter (uint32, zero-initialised once, plain memory).
+ * F1 runs on exactly the SM count of CTAs on every rank (all ranks: the same GPU model and the
+ * same nt), each flushing its counts with multimem.red and then signalling its counter
+ * (release, system scope); a one-CTA wait kernel then blocks the stream until every counter
+ * reached nranks x epoch (acquire).  After it, the local view of the buffer holds the global
+ * counts on every rank -- exact (integer).  No host synchronisation.  Requires NVLS multicast
+ * support; callers without it use edkm_uniquify + an all-reduce.
+ *   emulate   : 1 = the same protocol on ordinary device memory with plain atomics (nranks
+ *               must be 1; `*_mc` are then the buffers themselves) -- for testing the
+ *               protocol on a system without multicast.  0 otherwise. */
+#define EDKM_NVLS_FLAGS 1024
+typedef struct {
+    int32_t* counts_mc;
+    uint32_t* flags_mc;
+    const uint32_t* flags;
+    uint32_t* epoch;
+    int nranks;
+    int emulate;
+} edkm_nvls;
+edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* nvls, void* stream);
+
+/* NVLS multicast buffers backing edkm_nvls (driver-API plumbing; no compute).
+ *   edkm_mc_supported : *supported = 1 if the current device supports multicast objects.
+ *   edkm_mc_create    : rank 0 -- a multicast object of >= bytes for nranks GPUs (size rounded
+ *                       up to the multicast granularity, see edkm_mc_bytes); with export_fd it
+ *                       also returns a POSIX file descriptor to pass to the other ranks.
+ *   edkm_mc_import    : other ranks -- the object from that descriptor (dup'ed into this
+ *                       process), bytes = edkm_mc_bytes of rank 0's object.
+ *   edkm_mc_add_device: every rank, for its current device; all ranks must have added their
+ *                       device before any rank calls edkm_mc_bind (a barrier in between).
+ *   edkm_mc_bind      : backs the object with this rank's device memory and maps the unicast
+ *                       (*local_out) and multicast (*mc_out) views, both bytes long.
+ *   edkm_mc_destroy   : unmaps and releases (after all use; ranks tear down independently).
+ * The library owns nothing else; these are the only calls that allocate device memory. */
+typedef struct edkm_mcbuf edkm_mcbuf;
+edkm_status edkm_mc_supported(int* supported);
+edkm_status edkm_mc_create(size_t bytes, int nranks, int export_fd, int* fd_out, edkm_mcbuf** out);
+edkm_status edkm_mc_import(int fd, size_t bytes, edkm_mcbuf** out);
+size_t edkm_mc_bytes(const edkm_mcbuf* buf);
+edkm_status edkm_mc_add_device(edkm_mcbuf* buf);
+edkm_status edkm_mc_bind(edkm_mcbuf* buf, void** local_out, void** mc_out);
+edkm_status edkm_mc_destroy(edkm_mcbuf* buf);
+const char* edkm_mc_last_error(void);
 
 /* TF -- forward table phase (DKM iterations on the attention table).
  *   counts : [nt][65536] int32, global over ranks.

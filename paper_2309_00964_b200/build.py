@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "stream_kernels.cu", "table_kernels.cu", "table_wide.cu"]
+SOURCES = ["api.cu", "stream_kernels.cu", "table_kernels.cu", "table_wide.cu", "nvls.cu"]
 LIB = os.path.join(HERE, "libedkm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",

@@ -183,6 +183,36 @@ edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_
   return EDKM_OK;
 }
 
+edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* x, void* stream) {
+  g_launches = 0;
+  if (wdtype != EDKM_BF16 && wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");
+  edkm_status st = check_tensors(tensors, nt);
+  if (st != EDKM_OK) return st;
+  if (!x || !x->counts_mc || !x->flags_mc || !x->flags || !x->epoch) return fail(EDKM_E_ARG, "NULL NVLS buffer");
+  if (x->nranks < 1) return fail(EDKM_E_ARG, "nranks < 1");
+  if (x->emulate && x->nranks != 1) return fail(EDKM_E_ARG, "emulate requires nranks == 1");
+  if (nt > kMaxTensorsPerLaunch) return fail(EDKM_E_UNSUPPORTED, "NVLS uniquify takes at most 512 tensors per call");
+  const int sms = sm_count();
+  if (sms > EDKM_NVLS_FLAGS) return fail(EDKM_E_UNSUPPORTED, "more SMs than NVLS arrival counters");
+  static thread_local StreamArgs A;
+  A.wdtype = wdtype;
+  A.nt = nt;
+  A.t0 = 0;
+  A.offs[0] = 0;
+  for (int i = 0; i < nt; ++i) {
+    A.w[i] = reinterpret_cast<const uint16_t*>(tensors[i].w);
+    A.g[i] = nullptr;
+    A.out[i] = nullptr;
+    A.offs[i + 1] = A.offs[i] + tensors[i].n;
+  }
+  A.total = A.offs[nt];
+  cudaError_t e = launch_f1_nvls(A, x->counts_mc, x->flags_mc, x->flags, x->epoch, x->nranks, x->emulate, sms,
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "F1 NVLS histogram launch");
+  g_launches = 2;
+  return EDKM_OK;
+}
+
 edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
                          float* table, void* saved, void* stream) {
   g_launches = 0;

@@ -45,6 +45,8 @@ struct B2Args {
   const int64_t* page_cnt;  // [nt][256]
 };
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s);
+cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
+                           uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s);
 cudaError_t launch_f2(const StreamArgs& A, const F2Args& F, int mode, int sms, cudaStream_t s);
 cudaError_t launch_b1(const StreamArgs& A, const B1Args& B, int sms, cudaStream_t s);
 cudaError_t launch_b2(const StreamArgs& A, const B2Args& B, int sms, cudaStream_t s);

@@ -10,6 +10,8 @@
 // contiguous split of the concatenated weight space, 256-bit evict-first loads,
 // and the per-pattern table in shared memory.  No tensor cores: nothing here
 // is a contraction.
+#include <cstdio>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -87,6 +89,17 @@ __device__ __forceinline__ void for_each_segment(const StreamArgs& A, P& p) {
 __device__ __forceinline__ uint32_t pat(const V8& v, int e) { return (v.x[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu; }
 
 // ============================================================================ F1
+// Adds to the global counts: a plain L2 atomic, or (MC, NVLS mode) a multimem reduction on the
+// multicast address of a symmetric buffer -- the NVSwitch adds v into every rank's copy, so the
+// cross-rank sum of the counts happens inside F1's own flushes, with no separate collective.
+// MC = 0: plain; 1: NVLS multicast; 2: the same protocol on ordinary memory (one rank: tests).
+template <int MC>
+__device__ __forceinline__ void cnt_add(int32_t* p, int v) {
+  if (MC == 1) asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else atomicAdd(p, v);
+}
+
+template <int MC>
 struct F1Policy {
   static constexpr int kLoop = 1;  // two vectors per iteration (F1 is atomic-bound: more loads in flight)
   const StreamArgs& A;
@@ -103,7 +116,7 @@ struct F1Policy {
   __device__ void load(int t, int64_t i, Vec& r) const { r.w = ldg_stream8(A.w[t] + i); }
   __device__ void count(int t, uint32_t u) {
     if (u < (uint32_t)kF1Bins) red_shared_add(&h[u], 1u);
-    else atomicAdd(&cnt(t)[u], 1);
+    else cnt_add<MC>(&cnt(t)[u], 1);
   }
   __device__ void process(int t, int64_t, const Vec& r) {
 #pragma unroll
@@ -115,7 +128,7 @@ struct F1Policy {
     int32_t* c = cnt(t);
     for (int i = threadIdx.x; i < kF1Bins; i += blockDim.x) {
       const uint32_t v = h[i];
-      if (v) atomicAdd(&c[i], (int32_t)v);
+      if (v) cnt_add<MC>(&c[i], (int32_t)v);
     }
     __syncthreads();
   }
@@ -139,7 +152,8 @@ constexpr int kF1LRows = kF1LPages * 256;  // 1792 words per copy, 32 copies = 2
 constexpr int kF1LChunkVec = 127;          // vectors per thread between folds (32*127*16 < 65536)
 constexpr int kF1Sample = 16384;
 
-__device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u) { atomicAdd(&c[u], 1); }
+template <int MC>
+__device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u) { cnt_add<MC>(&c[u], 1); }
 
 // fold the 32 copies of rows tid and tid+1024 into acc (pos, neg per row) and zero them
 __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
@@ -164,8 +178,52 @@ __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
   }
 }
 
+template <int MC>
+__device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, uint32_t k16, uint32_t k128);
+
+// MC: NVLS mode -- `counts` is a multicast address; every CTA (the grid is exactly the SM count on
+// every rank) ends by adding 1 to its arrival counter flags_mc[blockIdx.x] with release semantics
+// at system scope, after its own flushes (see f1_nvls_wait_kernel).
+template <int MC>
 __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_constant__ StreamArgs A, int32_t* counts,
-                                                              uint32_t k16, uint32_t k128) {
+                                                              uint32_t k16, uint32_t k128, uint32_t* flags_mc) {
+  f1_body<MC>(A, counts, k16, k128);
+  if (MC) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (MC == 1) asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+      else asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+    }
+  }
+}
+
+// NVLS mode: wait until every CTA of every rank has arrived for this step (counter >= nranks *
+// epoch, monotonic, never reset, so a fast rank's next-step arrivals cannot be lost), then
+// advance this rank's epoch.  One CTA; the acquire loads order the reads of the counts after it.
+__global__ void f1_nvls_wait_kernel(const uint32_t* flags, int nflags, uint32_t* epoch, uint32_t nranks) {
+  const uint32_t e = *epoch + 1u, target = e * nranks;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int c = threadIdx.x; c < nflags; c += blockDim.x) {
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + c) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 20000000000ull) {  // 20 s: a rank is gone -- fail loudly instead of hanging
+        printf("edkm: NVLS arrival barrier timed out (counter %d = %u, waiting for %u)\n", c, v, target);
+        asm volatile("trap;");
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *epoch = e;
+}
+
+template <int MC>
+__device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, uint32_t k16, uint32_t k128) {
   extern __shared__ __align__(16) uint32_t smem_u32[];
   __shared__ uint32_t s_pg[kMagPages];
   __shared__ int s_base, s_lp;
@@ -175,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
   if (lo >= hi) return;
   int t = find_tensor(A, lo);
   const int tid = threadIdx.x, bs = blockDim.x, lane = tid & 31;
-  F1Policy gen{A, h, counts};
+  F1Policy<MC> gen{A, h, counts};
   while (lo < hi) {
     while (A.offs[t + 1] <= lo) ++t;
     const int64_t a = lo - A.offs[t], b = min(hi, A.offs[t + 1]) - A.offs[t];
@@ -216,8 +274,46 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
       const int64_t head = min((int64_t)(((32u - (uint32_t)(wa & 31u)) & 31u) >> 1), b - a);
       const int64_t va = a + head;
       const int64_t nv = (b - va) >> 4;
-      for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global(cnt, w[i]);
-      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global(cnt, w[i]);
+      for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global<MC>(cnt, w[i]);
+      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global<MC>(cnt, w[i]);
+      // one 16-pattern vector: lane-private increments, or per element when it leaves the window
+      auto count_vec = [&](const V8& r) {
+        uint32_t rel[8], rmax2 = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          rel[q] = __vadd2(r.x[q] & 0x7FFF7FFFu, pb2);
+          rmax2 = __vmaxu2(rmax2, rel[q]);
+        }
+        if (max(rmax2 & 0xFFFFu, rmax2 >> 16) < (uint32_t)kF1LRows) {
+          // Per 16-bit pair: row offsets by IMAD (k16, k128 are kernel parameters, opaque to
+          // ptxas, so the multiplies stay on the FMA pipe); the increment 1 or 0x10000 (sign of
+          // the pattern selects the counter half) from one PRMT sign-replicate + 1.  F1 is
+          // ALU-pipe bound otherwise (ncu: ALU 83%, FMA-heavy 34%).
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t x = r.x[q];
+            const uint32_t rh = __umulhi(rel[q], k16);
+            const uint32_t rl = rel[q] & 0xFFFFu;
+            uint32_t mlo, mhi;
+            asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));  // 0xFFFF if bit 15 set
+            asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));  // 0xFFFF if bit 31 set
+            red_add_shared(rl * k128 + base, mlo + 1u);
+            red_add_shared(rh * k128 + base, mhi + 1u);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t x = r.x[q];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const uint32_t rr = e ? (rel[q] >> 16) : (rel[q] & 0xFFFFu);
+              const uint32_t u = e ? (x >> 16) : (x & 0xFFFFu);
+              if (rr < (uint32_t)kF1LRows) red_add_shared(base + (rr << 7), 1u + (u >> 15) * 0xFFFFu);
+              else f1_count_global<MC>(cnt, u);
+            }
+          }
+        }
+      };
       for (int64_t c0 = 0; c0 < nv; c0 += (int64_t)kF1LChunkVec * bs) {
         const int64_t c1 = min(nv, c0 + (int64_t)kF1LChunkVec * bs);
 #pragma unroll 1
@@ -226,45 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
           const bool two = v + bs < c1;
           r[0] = ldg_stream8(w + va + 16 * v);
           if (two) r[1] = ldg_stream8(w + va + 16 * (v + bs));
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            if (k == 1 && !two) break;
-            uint32_t rel[8], rmax2 = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              rel[q] = __vadd2(r[k].x[q] & 0x7FFF7FFFu, pb2);
-              rmax2 = __vmaxu2(rmax2, rel[q]);
-            }
-            if (max(rmax2 & 0xFFFFu, rmax2 >> 16) < (uint32_t)kF1LRows) {
-              // Per 16-bit pair: row offsets by IMAD (k16, k128 are kernel parameters, opaque to
-              // ptxas, so the multiplies stay on the FMA pipe); the increment 1 or 0x10000 (sign of
-              // the pattern selects the counter half) from one PRMT sign-replicate + 1.  F1 is
-              // ALU-pipe bound otherwise (ncu: ALU 83%, FMA-heavy 34%).
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const uint32_t x = r[k].x[q];
-                const uint32_t rh = __umulhi(rel[q], k16);
-                const uint32_t rl = rel[q] & 0xFFFFu;
-                uint32_t mlo, mhi;
-                asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));  // 0xFFFF if bit 15 set
-                asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));  // 0xFFFF if bit 31 set
-                red_add_shared(rl * k128 + base, mlo + 1u);
-                red_add_shared(rh * k128 + base, mhi + 1u);
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const uint32_t x = r[k].x[q];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const uint32_t rr = e ? (rel[q] >> 16) : (rel[q] & 0xFFFFu);
-                  const uint32_t u = e ? (x >> 16) : (x & 0xFFFFu);
-                  if (rr < (uint32_t)kF1LRows) red_add_shared(base + (rr << 7), 1u + (u >> 15) * 0xFFFFu);
-                  else f1_count_global(cnt, u);
-                }
-              }
-            }
-          }
+          count_vec(r[0]);
+          if (two) count_vec(r[1]);
         }
         __syncthreads();
         f1l_fold(h, acc);
@@ -276,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
         const int r = tid + j * 1024;
         if (r < kF1LRows) {
           const uint32_t u = ((uint32_t)s_base << 8) + (uint32_t)r;
-          if (acc[2 * j]) atomicAdd(&cnt[u], (int32_t)acc[2 * j]);
-          if (acc[2 * j + 1]) atomicAdd(&cnt[u | 0x8000u], (int32_t)acc[2 * j + 1]);
+          if (acc[2 * j]) cnt_add<MC>(&cnt[u], (int32_t)acc[2 * j]);
+          if (acc[2 * j + 1]) cnt_add<MC>(&cnt[u | 0x8000u], (int32_t)acc[2 * j + 1]);
         }
       }
       __syncthreads();
@@ -291,14 +350,14 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
       for (int64_t i = a + tid; i < a + head; i += bs) gen.scalar(t, i);
       int64_t v = tid;
       for (; v + bs < nv; v += 2 * bs) {
-        F1Policy::Vec r0, r1;
+        typename F1Policy<MC>::Vec r0, r1;
         gen.load(t, va + 16 * v, r0);
         gen.load(t, va + 16 * (v + bs), r1);
         gen.process(t, va + 16 * v, r0);
         gen.process(t, va + 16 * (v + bs), r1);
       }
       if (v < nv) {
-        F1Policy::Vec r0;
+        typename F1Policy<MC>::Vec r0;
         gen.load(t, va + 16 * v, r0);
         gen.process(t, va + 16 * v, r0);
       }
@@ -757,9 +816,25 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s) {
   if (A.total == 0) return cudaSuccess;
   const size_t smem = kF1Bins * sizeof(uint32_t);
-  cudaError_t e = set_smem((const void*)f1_hist_kernel, smem);
+  cudaError_t e = set_smem((const void*)f1_hist_kernel<0>, smem);
   if (e != cudaSuccess) return e;
-  f1_hist_kernel<<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, 0x10000u, 128u);
+  f1_hist_kernel<0><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, 0x10000u, 128u, nullptr);
+  return cudaGetLastError();
+}
+
+// NVLS mode: grid = `sms` CTAs on every rank (also when this rank's slice is empty), each
+// signalling its arrival counter; then the wait kernel.
+cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
+                           uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s) {
+  const size_t smem = kF1Bins * sizeof(uint32_t);
+  const void* fn = emulate ? (const void*)f1_hist_kernel<2> : (const void*)f1_hist_kernel<1>;
+  cudaError_t e = set_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  if (emulate) f1_hist_kernel<2><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
+  else f1_hist_kernel<1><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  f1_nvls_wait_kernel<<<1, 256, 0, s>>>(flags, sms, epoch, (uint32_t)nranks);
   return cudaGetLastError();
 }
 

@@ -11,11 +11,20 @@ real exchange steps, both all-reduces over the process group (NCCL on B200):
 
 Nothing else crosses ranks: W~ and dW are produced for the local slice only, C_T
 and dC_0 come out identical on every rank.
+
+On NVSwitch systems with NVLS multicast, exchange 1 is fused into F1 itself
+(`NvlsCounts` + edkm_uniquify_nvls): F1's shared-memory flushes are multimem
+reductions into a symmetric buffer, summed by the switch into every rank's copy, and
+an in-kernel arrival barrier replaces the collective.  Exchange 2 (fp64) stays an
+NCCL all-reduce, whose result is bit-identical on every rank (in-switch fp64 adds
+would arrive in a different order on each GPU).
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+
+NVLS_FLAGS = 1024  # edkm.h EDKM_NVLS_FLAGS
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple:
@@ -44,17 +53,189 @@ class ShardedStep:
     B200 it is paper_2309_00964_b200.edkm.Plan.
     """
 
-    def __init__(self, kernels, group=None, allreduce=None):
+    def __init__(self, kernels, group=None, allreduce=None, nvls=None):
         self.k = kernels
         self.group = group
         self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
+        self.nvls = nvls
 
     def __call__(self, weights, grads, C0, outs, dW):
-        self.k.uniquify(weights)
-        self.allreduce(self.k.counts)                     # exchange 1: integer counts
+        if self.nvls is not None:
+            self.k.uniquify_nvls(weights, self.nvls)      # exchange 1 fused into F1 (NVSwitch)
+        else:
+            self.k.uniquify(weights)
+            self.allreduce(self.k.counts)                 # exchange 1: integer counts
         self.k.forward(C0)
         self.k.reconstruct(weights, outs)
         self.k.backward_reduce(weights, grads)
         self.allreduce(self.k.gamma)                      # exchange 2: gamma_T partials
         self.k.backward_apply(weights, grads, dW)
         return self.k.dC0
+
+
+class NvlsUnavailable(RuntimeError):
+    pass
+
+
+class _CudaArray:
+    """Zero-copy torch view of raw device memory (the __cuda_array_interface__ protocol)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _send_fd(name: str, fd: int, npeers: int, timeout: float = 120.0):
+    import socket
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind("\0" + name)
+    srv.listen(npeers)
+    srv.settimeout(timeout)
+    try:
+        for _ in range(npeers):
+            c, _ = srv.accept()
+            with c:
+                socket.send_fds(c, [b"x"], [fd])
+    finally:
+        srv.close()
+
+
+def _recv_fd(name: str, timeout: float = 120.0) -> int:
+    import socket
+    import time
+    t0 = time.time()
+    while True:
+        c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        try:
+            c.connect("\0" + name)
+            break
+        except OSError:
+            c.close()
+            if time.time() - t0 > timeout:
+                raise
+            time.sleep(0.01)
+    with c:
+        _, fds, _, _ = socket.recv_fds(c, 1, 1)
+    return fds[0]
+
+
+class NvlsCounts:
+    """NVLS buffers of the fused count exchange (include/edkm.h edkm_uniquify_nvls).
+
+    One multicast object (edkm_mc_*: driver-API plumbing in the library) holds two [nt][65536]
+    int32 count buffers used on alternate steps -- the one of the next step is zeroed before
+    this step's F1, so no rank can add into a copy another rank has not cleared -- and
+    NVLS_FLAGS monotonic arrival counters; plus this rank's epoch.  Rank 0 creates the object
+    and passes its file descriptor to the other ranks over a local socket (SCM_RIGHTS).
+    Raises NvlsUnavailable when the system has no NVLS multicast.  emulate=True (one rank
+    only) runs the same protocol -- kernels, epochs, alternating buffers -- on ordinary
+    device memory with plain atomics, to test it where multicast objects cannot be created.
+    """
+
+    def __init__(self, nt: int, device, group=None, emulate: bool = False):
+        import ctypes
+        import os
+        import uuid
+
+        from . import edkm as E
+        L = E.lib()
+        self.group = group
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = torch.device(device)
+        torch.cuda.set_device(dev)
+        self.emulate = bool(emulate)
+        self._nt = nt
+        self.step_index = 0
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.emulate:
+            if self.nranks != 1:
+                raise ValueError("emulate requires a single rank")
+            self._buf = None
+            self.bufs = [torch.zeros((max(nt, 1), 65536), dtype=torch.int32, device=dev) for _ in range(2)]
+            self.flags = torch.zeros(NVLS_FLAGS, dtype=torch.int32, device=dev)
+            self.mc_ptrs = [t.data_ptr() for t in self.bufs] + [self.flags.data_ptr()]
+            self.current = self.bufs[0][:nt]
+            return
+        sup = ctypes.c_int(0)
+        if L.edkm_mc_supported(ctypes.byref(sup)) != 0 or not sup.value:
+            ok = torch.zeros(1, device="cpu")
+        else:
+            ok = torch.ones(1, device="cpu")
+        if self.nranks > 1:
+            ok = self._all_min(ok)
+        if not ok.item():
+            raise NvlsUnavailable("no NVLS multicast support on this system")
+        self.nt = max(nt, 1)
+        cbytes = (self.nt * 65536 * 4 + 255) // 256 * 256
+        need = 2 * cbytes + NVLS_FLAGS * 4
+        buf = ctypes.c_void_p()
+        fd = ctypes.c_int(-1)
+        name = None
+        err = ""
+        if rank == 0:
+            rc = L.edkm_mc_create(ctypes.c_size_t(need), self.nranks, int(self.nranks > 1), ctypes.byref(fd),
+                                  ctypes.byref(buf))
+            if rc != 0:
+                err = L.edkm_mc_last_error().decode()
+            name = f"edkm-nvls-{os.getpid()}-{uuid.uuid4().hex}"
+        info = [name, int(L.edkm_mc_bytes(buf)) if buf.value else 0, err]
+        if self.nranks > 1:
+            dist.broadcast_object_list(info, src=0, group=group)
+        name, size, err = info
+        if not size:
+            raise NvlsUnavailable(f"multicast object creation failed: {err}")
+        if self.nranks > 1:
+            if rank == 0:
+                _send_fd(name, fd.value, self.nranks - 1)
+                os.close(fd.value)
+            else:
+                rfd = _recv_fd(name)
+                rc = L.edkm_mc_import(rfd, ctypes.c_size_t(size), ctypes.byref(buf))
+                os.close(rfd)
+                if rc != 0:
+                    raise NvlsUnavailable(f"multicast import failed: {L.edkm_mc_last_error().decode()}")
+        self._buf = buf
+        if L.edkm_mc_add_device(buf) != 0:
+            raise NvlsUnavailable(f"cuMulticastAddDevice failed: {L.edkm_mc_last_error().decode()}")
+        if self.nranks > 1:
+            dist.barrier(group)
+        loc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        if L.edkm_mc_bind(buf, ctypes.byref(loc), ctypes.byref(mc)) != 0:
+            raise NvlsUnavailable(f"multicast bind failed: {L.edkm_mc_last_error().decode()}")
+        self.local, self.mcbase = loc.value, mc.value
+        self.offs = [0, cbytes, 2 * cbytes]
+        self.bufs = [torch.as_tensor(_CudaArray(self.local + o, (self.nt, 65536), "<i4"), device=dev)
+                     for o in self.offs[:2]]
+        self.flags = torch.as_tensor(_CudaArray(self.local + self.offs[2], (NVLS_FLAGS,), "<i4"), device=dev)
+        self.mc_ptrs = [self.mcbase + o for o in self.offs]
+        for t in self.bufs + [self.flags]:
+            t.zero_()
+        self.current = self.bufs[0][:nt]
+        torch.cuda.synchronize(dev)
+        if self.nranks > 1:
+            dist.barrier(group)
+
+    def _all_min(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return t
+
+    def next_step(self, stream=None):
+        """C struct for this step's call; zeroes the next step's buffer on `stream` first."""
+        from . import edkm as E
+        s = self.step_index
+        self.step_index += 1
+        cur, nxt = s % 2, (s + 1) % 2
+        with torch.cuda.stream(stream or torch.cuda.current_stream()):
+            self.bufs[nxt].zero_()
+        self.current = self.bufs[cur][:self._nt]
+        return E._Nvls(self.mc_ptrs[cur], self.mc_ptrs[2], self.flags.data_ptr(), self.epoch.data_ptr(), self.nranks,
+                       int(self.emulate))
+
+    def close(self):
+        from . import edkm as E
+        if getattr(self, "_buf", None) is not None and self._buf.value:
+            torch.cuda.synchronize()
+            self.bufs = self.flags = self.current = None
+            E.lib().edkm_mc_destroy(self._buf)
+            self._buf = None

@@ -42,6 +42,14 @@ class _Tensor(ctypes.Structure):
     _fields_ = [("w", ctypes.c_void_p), ("n", ctypes.c_int64)]
 
 
+class _Nvls(ctypes.Structure):
+    _fields_ = [("counts_mc", ctypes.c_void_p), ("flags_mc", ctypes.c_void_p), ("flags", ctypes.c_void_p),
+                ("epoch", ctypes.c_void_p), ("nranks", ctypes.c_int), ("emulate", ctypes.c_int)]
+
+
+NVLS_FLAGS = 1024
+
+
 class _Params(ctypes.Structure):
     _fields_ = [("wdtype", ctypes.c_int), ("bits", ctypes.c_int), ("tau", ctypes.c_double),
                 ("max_iter", ctypes.c_int), ("eps", ctypes.c_double)]
@@ -64,6 +72,7 @@ def lib():
             "edkm_saved_bytes": ([i32, pp], ctypes.c_size_t),
             "edkm_workspace_bytes": ([i32, pp], ctypes.c_size_t),
             "edkm_uniquify": ([P, i32, i32, P, P], i32),
+            "edkm_uniquify_nvls": ([P, i32, i32, ctypes.POINTER(_Nvls), P], i32),
             "edkm_forward": ([P, i32, pp, P, P, P, P, P], i32),
             "edkm_reconstruct": ([P, i32, pp, P, P, P, i32, i32, P, P], i32),
             "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P], i32),
@@ -75,6 +84,14 @@ def lib():
             "edkm_backward_dw": ([P, i32, pp, P, i32, P, P, P, i32, P], i32),
             "edkm_read_status": ([P, i32, pp, P, P, P], i32),
             "edkm_last_launch_count": ([], i32),
+            "edkm_mc_supported": ([P], i32),
+            "edkm_mc_create": ([ctypes.c_size_t, i32, i32, P, P], i32),
+            "edkm_mc_import": ([i32, ctypes.c_size_t, P], i32),
+            "edkm_mc_bytes": ([P], ctypes.c_size_t),
+            "edkm_mc_add_device": ([P], i32),
+            "edkm_mc_bind": ([P, P, P], i32),
+            "edkm_mc_destroy": ([P], i32),
+            "edkm_mc_last_error": ([], ctypes.c_char_p),
             "edkm_set_max_ctas": ([i32], i32),
             "edkm_status_string": ([i32], ctypes.c_char_p),
             "edkm_last_error": ([], ctypes.c_char_p),
@@ -87,10 +104,12 @@ def lib():
 
 
 def exported_symbols() -> list:
-    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_forward", "edkm_reconstruct",
+    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_uniquify_nvls", "edkm_forward", "edkm_reconstruct",
             "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_backward_buckets",
             "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
-            "edkm_last_launch_count", "edkm_set_max_ctas", "edkm_status_string", "edkm_last_error"]
+            "edkm_last_launch_count", "edkm_set_max_ctas", "edkm_status_string", "edkm_last_error",
+            "edkm_mc_supported", "edkm_mc_create", "edkm_mc_import", "edkm_mc_bytes", "edkm_mc_add_device",
+            "edkm_mc_bind", "edkm_mc_destroy", "edkm_mc_last_error"]
 
 
 def _check(rc: int, what: str):
@@ -292,6 +311,15 @@ class Plan:
     def uniquify(self, weights, stream=None):
         _check(lib().edkm_uniquify(self._arr("w", weights, _tensor_array), self.nt, _DT[self.p.wdtype],
                                    _ptr(self.counts), _stream(stream)), "edkm_uniquify")
+        return self.counts
+
+    def uniquify_nvls(self, weights, nvls, stream=None):
+        """F1 with the cross-rank count sum done in the NVSwitch (edkm_uniquify_nvls); `nvls` is a
+        dist.NvlsCounts.  Leaves self.counts = this step's local view of the global counts."""
+        x = nvls.next_step()
+        _check(lib().edkm_uniquify_nvls(self._arr("w", weights, _tensor_array), self.nt, _DT[self.p.wdtype],
+                                        ctypes.byref(x), _stream(stream)), "edkm_uniquify_nvls")
+        self.counts = nvls.current
         return self.counts
 
     def forward(self, C0, stream=None):

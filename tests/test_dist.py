@@ -152,3 +152,37 @@ def test_world_size_2_gloo_matches_single_process_oracle():
         got_dW = np.concatenate([res[r][2][t] for r in range(world)])
         assert np.max(np.abs(got_Wt - Wt)) <= 1e-10 * np.max(np.abs(Wt)), (t, np.max(np.abs(got_Wt - Wt)))
         assert np.max(np.abs(got_dW - dW)) <= 1e-10 * np.max(np.abs(dW))
+
+
+def _fd_peer(name, q):
+    from paper_2309_00964_b200.dist import _recv_fd
+    fd = _recv_fd(name, timeout=30)
+    with os.fdopen(fd, "rb") as f:
+        q.put(f.read())
+
+
+def test_nvls_handle_passing_between_processes():
+    """NvlsCounts' plumbing: rank 0's multicast-object file descriptor reaches the other ranks
+    over an abstract local socket (SCM_RIGHTS); here a pipe's read end stands in for it."""
+    import multiprocessing as mpm
+    import uuid
+
+    from paper_2309_00964_b200.dist import _send_fd
+    ctx = mpm.get_context("spawn")
+    q = ctx.Queue()
+    name = f"edkm-test-{uuid.uuid4().hex}"
+    peers = [ctx.Process(target=_fd_peer, args=(name, q)) for _ in range(2)]
+    for p in peers:
+        p.start()
+    r, w = os.pipe()
+    os.write(w, b"multicast handle")
+    os.close(w)
+    try:
+        _send_fd(name, r, 2, timeout=30)
+    finally:
+        os.close(r)
+    got = [q.get(timeout=30) for _ in peers]
+    for p in peers:
+        p.join(timeout=30)
+    # both peers hold a duplicate of the same pipe: the bytes are read once in total
+    assert sorted(got) == sorted([b"multicast handle", b""])

@@ -97,3 +97,65 @@ def test_two_ranks_on_one_gpu_match_single_process_oracle():
         gdW = np.concatenate([res[r][5][t] for r in range(world)])
         assert np.max(np.abs(gWt - Wt)) <= TOL * np.max(np.abs(Wt))
         assert np.max(np.abs(gdW - dW)) <= TOL * np.max(np.abs(dW))
+
+
+def _nvls_worker(port, q, emulate):
+    """World size 1 over NCCL on the one B200: the NVLS-fused F1 (multimem reductions into a
+    symmetric buffer + in-kernel arrival barrier) against plain F1, over several steps (the two
+    alternating count buffers and the monotonic epoch), plus one ShardedStep with it."""
+    from paper_2309_00964_b200.dist import NvlsCounts, NvlsUnavailable
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        p = E.Params(torch.bfloat16, **P_)
+        try:
+            nv = NvlsCounts(len(SIZES), dev, emulate=emulate)
+        except NvlsUnavailable as e:
+            q.put(("skip", str(e)))
+            return
+        plan = E.Plan(SIZES, p, dev)
+        ref = E.Plan(SIZES, p, dev)
+        res = []
+        for step in range(5):
+            Ws = [synth.normal_tensor(n, 1.0 + step, torch.bfloat16, 700 + 10 * step + i).to(dev)
+                  for i, n in enumerate(SIZES)]
+            if step == 3:  # an fp16-like spread: the shared-array path of F1
+                Ws[0] = torch.randint(0, 65536, (SIZES[0],), dtype=torch.int32).to(torch.int16).view(torch.bfloat16).to(dev)
+            got = plan.uniquify_nvls(Ws, nv).clone()
+            want = ref.uniquify(Ws).clone()
+            torch.cuda.synchronize()
+            res.append(bool(torch.equal(got, want)))
+        Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 800 + i).to(dev) for i, n in enumerate(SIZES)]
+        Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 900 + i).to(dev) for i, n in enumerate(SIZES)]
+        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
+        outs = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        dW = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        outs2 = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        dW2 = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        ShardedStep(plan, nvls=nv)(Ws, Gs, C0, outs, dW)
+        ref.step(Ws, Gs, C0, outs2, dW2)
+        torch.cuda.synchronize()
+        same = all(torch.equal(a, b) for a, b in zip(outs + dW, outs2 + dW2)) and torch.equal(plan.dC0, ref.dC0)
+        q.put(("ok", res, bool(same), int(nv.epoch.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("emulate", [True, False])
+def test_nvls_fused_counts_world1(emulate):
+    """emulate=False needs a system where multicast objects can be created (skips otherwise);
+    emulate=True runs the identical kernels/protocol with plain atomics on ordinary memory."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nvls_worker, args=(free_port(), q, emulate))
+    pr.start()
+    out = q.get(timeout=600)
+    pr.join(timeout=120)
+    if out[0] == "skip":
+        pytest.skip(out[1])
+    _, res, same, epoch = out
+    assert all(res), res
+    assert same
+    assert epoch == 6  # five uniquify_nvls steps + the ShardedStep
