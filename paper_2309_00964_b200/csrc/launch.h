@@ -12,11 +12,12 @@ constexpr int kMaxCluster = 8;
 struct TensorState {
   int32_t T;                       // centroid updates run
   int32_t cl;                      // CTAs per tensor in the table phase (row partitions)
+  int32_t pbase[kMaxCluster + 1];  // partition p = patterns [pbase[p], pbase[p+1]) (16-aligned, row-balanced)
+  int32_t nrows[kMaxCluster];      // populated finite patterns, per partition (stored at rows[pbase[p]...])
+  int32_t pad0;
   int64_t nonfinite[kMaxCluster];  // NaN/Inf weights counted, per partition
-  int32_t nrows[kMaxCluster];      // populated finite patterns, per partition
-  int32_t pad[6];
 };
-static_assert(sizeof(TensorState) == 128, "TensorState layout");
+static_assert(sizeof(TensorState) == 144, "TensorState layout");
 
 struct SavedLayout {
   size_t state, ctraj, straj, rows, table16, idx8, page_cnt, total;

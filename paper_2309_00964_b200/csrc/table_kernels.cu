@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "table_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -186,25 +187,43 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
   __shared__ int s_scan[(kFThreads / 32)];
   __shared__ long long s_nf[(kFThreads / 32)];
 
+  __shared__ int s_pg[256], s_pref[257], s_pb[kMaxCluster + 1];
+
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
-  const int chunk = kPatterns / cl, base = crank * chunk;
-  uint16_t* rows = P.rows + (int64_t)t * kPatterns + base;
   TensorState* st = P.state + t;
   float* tab = P.table + (int64_t)t * kPatterns;
   uint16_t* tab16 = P.table16 + (int64_t)t * kPatterns;
   uint8_t* idx = P.idx8 + (int64_t)t * kPatterns;
 
+  // ---- 0. partition bounds (identical on every CTA): the two signs for cl = 2 (balanced for a
+  //         symmetric law, and page masses come from the compaction loop), else row-balanced ranges
+  //         (which also writes the page masses)
+  const bool sign_split = cl == 2;
+  if (sign_split) {
+    if (tid == 0) {
+      s_pb[0] = 0;
+      s_pb[1] = kPatterns / 2;
+      s_pb[2] = kPatterns;
+    }
+    __syncthreads();
+  } else {
+    table_partitions<kFThreads>(cnt, P.wdtype, P.page_cnt + (int64_t)t * 256, cl, crank, cluster, s_pg, s_pref, s_pb);
+  }
+  const int base = s_pb[crank], end = s_pb[crank + 1];
+  uint16_t* rows = P.rows + (int64_t)t * kPatterns + base;
+
   // ---- 1. compact populated finite patterns of this partition (ascending u), 16 per thread per step;
-  //         page masses (every present pattern), non-finite counts, NaN-fill of the W~ tables
+  //         non-finite counts, NaN-fill of the W~ tables
   int nr = 0;
   long long nonfin = 0;
-  for (int off = 0; off < chunk; off += kFThreads * 16) {
+  for (int off = 0; off < end - base; off += kFThreads * 16) {
     const int u0 = base + off + tid * 16;
+    const bool in = u0 < end;
     int c[16];
-    const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
+    const int4* c4 = reinterpret_cast<const int4*>(cnt + (in ? u0 : 0));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int4 x = __ldg(c4 + q);
+      const int4 x = in ? __ldg(c4 + q) : make_int4(0, 0, 0, 0);
       c[4 * q] = x.x;
       c[4 * q + 1] = x.y;
       c[4 * q + 2] = x.z;
@@ -219,20 +238,23 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
       if (!fin) nonfin += c[e];
       pm += c[e];
     }
-    // NaN fill (populated entries are overwritten in phase 3); hard index 0 for non-finite patterns
-    const float nanf = __int_as_float(0x7FC00000);
-    float4* t4 = reinterpret_cast<float4*>(tab + u0);
+    if (sign_split) {  // one signed page = 256 patterns = 16 threads (the ranges are page-aligned)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) t4[q] = make_float4(nanf, nanf, nanf, nanf);
-    const uint32_t n16 = nan16(P.wdtype) * 0x10001u;
-    uint4* h4 = reinterpret_cast<uint4*>(tab16 + u0);
-    h4[0] = make_uint4(n16, n16, n16, n16);
-    h4[1] = make_uint4(n16, n16, n16, n16);
-    *reinterpret_cast<uint4*>(idx + u0) = make_uint4(0, 0, 0, 0);  // populated entries set in phase 3
-    // one signed page = 256 patterns = 16 threads
+      for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
+      if ((lane & 15) == 0) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
+    }
+    if (in) {
+      // NaN fill (populated entries are overwritten in phase 3); hard index 0 for non-finite patterns
+      const float nanf = __int_as_float(0x7FC00000);
+      float4* t4 = reinterpret_cast<float4*>(tab + u0);
 #pragma unroll
-    for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
-    if ((lane & 15) == 0) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
+      for (int q = 0; q < 4; ++q) t4[q] = make_float4(nanf, nanf, nanf, nanf);
+      const uint32_t n16 = nan16(P.wdtype) * 0x10001u;
+      uint4* h4 = reinterpret_cast<uint4*>(tab16 + u0);
+      h4[0] = make_uint4(n16, n16, n16, n16);
+      h4[1] = make_uint4(n16, n16, n16, n16);
+      *reinterpret_cast<uint4*>(idx + u0) = make_uint4(0, 0, 0, 0);  // populated entries set in phase 3
+    }
     // block exclusive scan of the per-thread populated counts
     const int np = __popc(popmask);
     int incl = np;
@@ -267,7 +289,10 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
     for (int w = 0; w < (kFThreads / 32); ++w) s += s_nf[w];
     st->nonfinite[crank] = s;
     st->nrows[crank] = nr;
-    if (crank == 0) st->cl = cl;
+    if (crank == 0) {
+      st->cl = cl;
+      for (int r = 0; r <= cl; ++r) st->pbase[r] = s_pb[r];
+    }
   }
   RowStage R{rows, cnt, reinterpret_cast<float*>(stage_mem), reinterpret_cast<int32_t*>(stage_mem) + kStage, nullptr,
              nullptr, nr, P.wdtype};
@@ -370,7 +395,7 @@ __global__ void __launch_bounds__(kFThreads) tgamma_kernel(const TableArgs P) {
 #pragma unroll
   for (int l = 0; l < K; ++l) acc[l] = 0.0;
   for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * (kPatterns / pcl);
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
     const int nr = st->nrows[p];
     for (int r = tid; r < nr; r += kFThreads) {
       const uint32_t u = rows[r];
@@ -412,9 +437,9 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   // this CTA owns partitions p = crank, crank + cl, ...; with pcl == cl (always, same
   // heuristic in TF) that is the single partition `crank`, staged in shared memory
   const bool one = pcl == cl;
-  const int chunk = kPatterns / pcl;
-  RowStage R{P.rows + (int64_t)t * kPatterns + crank * chunk, cnt, reinterpret_cast<float*>(stage_mem + kStage),
-             reinterpret_cast<int32_t*>(stage_mem + kStage) + kStage, stage_mem, psi + crank * chunk,
+  const int pb0 = one ? st->pbase[crank] : 0;
+  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem + kStage),
+             reinterpret_cast<int32_t*>(stage_mem + kStage) + kStage, stage_mem, psi + pb0,
              one ? st->nrows[crank] : 0, P.wdtype};
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
@@ -437,8 +462,8 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
 #pragma unroll
     for (int l = 0; l < K; ++l) acc[l] = 0.0;
     for (int p = crank; p < pcl; p += cl) {
-      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
-      double* gpsi = psi + p * chunk;
+      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+      double* gpsi = psi + st->pbase[p];
       const int nr = one ? R.nr : st->nrows[p];
       for (int r = tid; r < nr; r += kBThreads) {
         const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
@@ -475,8 +500,8 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   __syncthreads();
   float2* pp = P.phipsi + (int64_t)t * kPatterns;
   for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
-    double* gpsi = psi + p * chunk;
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+    double* gpsi = psi + st->pbase[p];
     const int nr = one ? R.nr : st->nrows[p];
     for (int r = tid; r < nr; r += kBThreads) {
       const uint32_t u = rows[r];
@@ -495,7 +520,7 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
     // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN.
     // 16 patterns per thread per step (vector loads of the counts).
     const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
-    for (int u0 = p * chunk + tid * 16; u0 < (p + 1) * chunk; u0 += kBThreads * 16) {
+    for (int u0 = st->pbase[p] + tid * 16; u0 < st->pbase[p + 1]; u0 += kBThreads * 16) {
       const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
       int c[16];
 #pragma unroll
@@ -515,9 +540,11 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
 }
 
 // ============================================================================ launchers
-// CTAs per tensor: fill the GPU for small nt; at least 2 (the positive and negative
-// pattern halves, which split a symmetric weight distribution evenly) so a CTA stages
-// at most 32K rows
+// CTAs per tensor (row partitions, <= the portable cluster size 8): fill the GPU for small nt,
+// else 2.  Rows are balanced across the partitions, but each CTA pays fixed costs per iteration
+// (centroid tables, cluster reduction), and a CTA left alone on an SM in a partial last wave runs
+// faster, so more, smaller partitions measured slower for 226 tensors (cl = 5: TF 0.15 -> 0.26 ms,
+// TB 0.27 -> 0.47 ms on CFG3; CFG4 also slower) -- wave quantisation is not the limit here.
 int table_cluster_size(int nt) {
   if (nt <= 18) return 8;
   if (nt <= 37) return 4;

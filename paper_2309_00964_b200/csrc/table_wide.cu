@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "table_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -133,8 +134,10 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
   WideSmem<K>& S = *reinterpret_cast<WideSmem<K>*>(wsm);
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_pg[256], s_pref[257], s_pb[kMaxCluster + 1];
   const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
-  const int chunk = kPatterns / cl, base = crank * chunk;
+  table_partitions<kWThreads>(cnt, P.wdtype, P.page_cnt + (int64_t)t * 256, cl, crank, cluster, s_pg, s_pref, s_pb);
+  const int base = s_pb[crank], end = s_pb[crank + 1];
   uint16_t* rows = P.rows + (int64_t)t * kPatterns + base;
   TensorState* st = P.state + t;
   float* tab = P.table + (int64_t)t * kPatterns;
@@ -142,23 +145,23 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
   uint8_t* idx = P.idx8 + (int64_t)t * kPatterns;
   const float nanf = __int_as_float(0x7FC00000);
 
-  // ---- 1. compaction (one pattern per thread per step), page masses, NaN fill
+  // ---- 1. compaction of this partition (one pattern per thread per step), NaN fill
   int nr = 0;
   long long nonfin = 0;
-  for (int off = 0; off < chunk; off += kWThreads) {
+  for (int off = 0; off < end - base; off += kWThreads) {
     const int u = base + off + tid;
-    const int c = cnt[u];
+    const bool in = u < end;
+    const int c = in ? cnt[u] : 0;
     const bool fin = pattern_finite(u, P.wdtype);
-    const bool pop = fin && c > 0;
+    const bool pop = in && fin && c > 0;
     if (!fin) nonfin += c;
-    idx[u] = 0;  // populated entries set in phase 3
-    tab[u] = nanf;
-    tab16[u] = nan16(P.wdtype);
+    if (in) {
+      idx[u] = 0;  // populated entries set in phase 3
+      tab[u] = nanf;
+      tab16[u] = nan16(P.wdtype);
+    }
     const unsigned b = __ballot_sync(0xffffffffu, pop);
-    long long pm = c;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
-    if (lane == 0) { S.scan[warp] = __popc(b); S.nf[warp] = pm; }
+    if (lane == 0) S.scan[warp] = __popc(b);
     __syncthreads();
     int woff = 0, btot = 0;
     for (int w = 0; w < kWWarps; ++w) {
@@ -166,11 +169,6 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
       btot += S.scan[w];
     }
     if (pop) rows[nr + woff + __popc(b & ((1u << lane) - 1u))] = (uint16_t)u;
-    if (tid < kWThreads / 256) {
-      long long s = 0;
-      for (int w = 0; w < 8; ++w) s += S.nf[tid * 8 + w];
-      P.page_cnt[(int64_t)t * 256 + ((base + off) >> 8) + tid] = s;
-    }
     nr += btot;
     __syncthreads();
   }
@@ -183,7 +181,10 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
     for (int w = 0; w < kWWarps; ++w) s += S.nf[w];
     st->nonfinite[crank] = s;
     st->nrows[crank] = nr;
-    if (crank == 0) st->cl = cl;
+    if (crank == 0) {
+      st->cl = cl;
+      for (int r = 0; r <= cl; ++r) st->pbase[r] = s_pb[r];
+    }
   }
   for (int r = tid; r < nr && r < kWStage; r += kWThreads) {
     const uint32_t u = rows[r];
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kWThreads) tgamma_wide_kernel(const TableArgs 
 #pragma unroll
   for (int q = 0; q < J; ++q) acc[0][q] = 0.0;
   for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * (kPatterns / pcl);
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
     const int nr = st->nrows[p];
     for (int r = warp; r < nr; r += kWWarps) {
       const uint32_t u = rows[r];
@@ -346,9 +347,8 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
   const double* ctraj = P.ctraj + (int64_t)t * (P.max_iter + 1) * K;
   const double* straj = P.straj + (int64_t)t * (P.max_iter > 0 ? P.max_iter : 1) * K;
   double* psi = P.psi + (int64_t)t * kPatterns;
-  const int chunk = kPatterns / pcl;
   const bool one = pcl == cl;
-  const uint16_t* rows0 = P.rows + (int64_t)t * kPatterns + crank * chunk;
+  const uint16_t* rows0 = P.rows + (int64_t)t * kPatterns + (one ? st->pbase[crank] : 0);
   const int nr0 = one ? st->nrows[crank] : 0;
   for (int r = tid; r < nr0 && r < kWStage; r += kWThreads) {
     const uint32_t u = rows0[r];
@@ -370,8 +370,8 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
 #pragma unroll
     for (int q = 0; q < J; ++q) acc[0][q] = 0.0;
     for (int p = crank; p < pcl; p += cl) {
-      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
-      double* gpsi = psi + p * chunk;
+      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+      double* gpsi = psi + st->pbase[p];
       const int nr = one ? nr0 : st->nrows[p];
       for (int r = warp; r < nr; r += kWWarps) {
         const bool staged = one && r < kWStage;
@@ -412,8 +412,8 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
   __syncthreads();
   float2* pp = P.phipsi + (int64_t)t * kPatterns;
   for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + p * chunk;
-    double* gpsi = psi + p * chunk;
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+    double* gpsi = psi + st->pbase[p];
     const int nr = one ? nr0 : st->nrows[p];
     for (int r = warp; r < nr; r += kWWarps) {
       const bool staged = one && r < kWStage;
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
         pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
       }
     }
-    for (int u = p * chunk + tid; u < (p + 1) * chunk; u += kWThreads)
+    for (int u = st->pbase[p] + tid; u < st->pbase[p + 1]; u += kWThreads)
       if (!pattern_finite(u, P.wdtype) || cnt[u] == 0)
         pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
   }
