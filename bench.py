@@ -238,10 +238,23 @@ def main():
         numels.append(hi - lo)
     n_local = sum(numels)
     n_total = wl.numel
+    # N > 1: split the table phase by tensor block when it is heavy (k T >= 64, e.g. CFG4's k=16, T=30):
+    # each rank runs TF/TB for its block, the ranks all-gather the per-tensor results (dist.ShardedStep)
+    tmode = os.environ.get("EDKM_SHARD_TABLE", "auto")
+    shard = tmode == "1" or (world > 1 and tmode == "auto" and wl.k * wl.max_iter >= 64)
+    if shard:
+        from paper_2309_00964_b200.dist import allgather_blocks, padded_numels
+        npad = len(padded_numels(numels, world)) - len(numels)
+        Ws += [torch.empty(0, dtype=wl.wdtype, device=dev)] * npad
+        Gs += [torch.empty(0, dtype=wl.wdtype, device=dev)] * npad
+        numels += [0] * npad
+        blk = len(numels) // world
+        t0, t1 = rank * blk, (rank + 1) * blk
     C0 = torch.tensor([synth.quantile_centroids(wl.k, wl.sigma)] * len(Ws), dtype=torch.float32, device=dev)
     Wt = [torch.empty_like(w) for w in Ws]
     dW = [torch.empty_like(w) for w in Ws]
     plan = E.Plan(numels, p, dev)
+    views = plan.views() if shard else None
     stream = torch.cuda.current_stream()
 
     def allreduce(t):
@@ -285,7 +298,12 @@ def main():
             mark(1)
             allreduce(plan.counts)           # exchange 1 (N > 1)
         mark(2)
-        plan.forward(C0)                     # TF
+        if shard:
+            plan.forward_range(t0, t1, C0)   # TF, this rank's tensor block
+            for name in ("state", "ctraj", "rows", "page_cnt", "C_out", "table16"):
+                allgather_blocks(views[name])
+        else:
+            plan.forward(C0)                 # TF
         mark(3)
         plan.reconstruct(Ws, Wt, E.SOFT)     # F2
         mark(4)
@@ -295,7 +313,12 @@ def main():
         mark(6)
         allreduce(plan.gamma)                # exchange 2 (N > 1)
         mark(7)
-        plan.backward_table()                # TB
+        if shard:
+            plan.backward_table_range(t0, t1)  # TB, this rank's tensor block
+            for name in ("phipsi", "dC0"):
+                allgather_blocks(views[name])
+        else:
+            plan.backward_table()            # TB
         mark(8)
         plan.backward_dw(Ws, Gs, dW)         # B2
         mark(9)
@@ -393,6 +416,7 @@ def main():
                                f"b={wl.bits} (k={wl.k}), tau={wl.tau}, T={wl.max_iter}",
                    "tensors": len(wl.shapes), "weights": n_total, "bits": wl.bits, "tau": wl.tau,
                    "iters": wl.max_iter, "parallelism": f"slices{world}", "exchange": exchange,
+                   "table_phase": "split by tensor block + all-gather" if shard else "replicated on every rank",
                    "arith": "bf16 I/O; fp32 per-weight passes; fp64 table phase",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
         "phases_ms": phase, "gpu_launches": launches_per_step * args.steps,

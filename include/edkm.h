@@ -154,6 +154,22 @@ const char* edkm_mc_last_error(void);
 edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
                          float* table, void* saved, void* stream);
 
+/* TF for tensors [t0, t1) of an nt-tensor call only (same buffers, same layout as edkm_forward,
+ * which is the range [0, nt)).  Lets ranks split the table phase by tensor (each rank runs TF
+ * for its own block, then the ranks exchange the per-tensor results, see edkm_layout) instead of
+ * all running it for every tensor.  Entries of other tensors are not touched. */
+edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p, const float* C0,
+                               float* C_out, float* table, void* saved, void* stream);
+
+/* Byte offsets of the arrays inside `saved` and `ws` for nt tensors (for exchanging per-tensor
+ * blocks between ranks).  Each array is [nt][per-tensor entries], tensor-major.
+ *   saved_offs[8] : TensorState (144 B/tensor), C trajectory (fp64 (max_iter+1)k), S trajectory
+ *                   (fp64 max(max_iter,1)k), rows (u16 65536), table16 (u16 65536), idx8 (u8
+ *                   65536), page_cnt (i64 256), total.
+ *   ws_offs[5]    : B (fp64 65536), psi (fp64 65536), (phi, psi) (float2 65536), gamma (fp64 k),
+ *                   total.  Either pointer may be NULL. */
+edkm_status edkm_layout(int nt, const edkm_params* p, size_t* saved_offs, size_t* ws_offs);
+
 /* F2 -- reconstruct this rank's slice of each tensor (Fig. 1, "look-up").
  *   table, C_out : the outputs of edkm_forward (table is read only by EDKM_SOFT with
  *                  FP32 output, C_out only by EDKM_HARD_VALUE; the other may be NULL).
@@ -201,6 +217,11 @@ edkm_status edkm_backward_table(int nt, const edkm_params* p, const int32_t* cou
 edkm_status edkm_backward_dw(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
                              int gdtype, const void* saved, const void* ws, void* const* dW, int dw_dtype,
                              void* stream);
+
+/* TB for tensors [t0, t1) only (see edkm_forward_range): (phi, psi) and dC0 of those tensors,
+ * from the global gamma.  Requires TF to have run for the same range on this rank. */
+edkm_status edkm_backward_table_range(int nt, int t0, int t1, const edkm_params* p, const int32_t* counts,
+                                      const void* saved, void* ws, const double* gamma, float* dC0, void* stream);
 
 /* Single-process convenience: edkm_backward_reduce then edkm_backward_apply with
  * `gamma` in ws.  Only valid when one process holds every weight of each tensor. */

@@ -123,6 +123,36 @@ void ws_args(TableArgs& P, void* ws) {
   P.phipsi = reinterpret_cast<float2*>(b + L.phipsi);
 }
 
+template <class T>
+T* off(T* p, int64_t n) { return p ? p + n : p; }
+
+// TableArgs built for nt tensors restricted to tensors [t0, t1): every per-tensor array pointer
+// advanced by t0 entries of the full-nt layout; the cluster size follows the range's count.
+TableArgs table_range(const TableArgs& P, int t0, int t1) {
+  TableArgs R = P;
+  const int64_t k = P.k, sc = (int64_t)(P.max_iter + 1) * k, ss = (int64_t)(P.max_iter > 0 ? P.max_iter : 1) * k;
+  const int64_t u = (int64_t)t0 * kPatterns;
+  R.nt = t1 - t0;
+  R.cl = table_cluster_size(R.nt);
+  R.counts = off(P.counts, u);
+  R.C0 = off(P.C0, t0 * k);
+  R.C_out = off(P.C_out, t0 * k);
+  R.table = off(P.table, u);
+  R.state = off(P.state, t0);
+  R.ctraj = off(P.ctraj, t0 * sc);
+  R.straj = off(P.straj, t0 * ss);
+  R.rows = off(P.rows, u);
+  R.table16 = off(P.table16, u);
+  R.idx8 = off(P.idx8, u);
+  R.page_cnt = off(P.page_cnt, (int64_t)t0 * 256);
+  R.B = off(P.B, u);
+  R.psi = off(P.psi, u);
+  R.phipsi = off(P.phipsi, u);
+  R.gamma = off(P.gamma, t0 * k);
+  R.dC0 = off(P.dC0, t0 * k);
+  return R;
+}
+
 }  // namespace
 
 namespace edkm {
@@ -213,23 +243,34 @@ edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, c
   return EDKM_OK;
 }
 
-edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
-                         float* table, void* saved, void* stream) {
+edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p, const float* C0,
+                               float* C_out, float* table, void* saved, void* stream) {
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
   if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
-  if (nt == 0) return EDKM_OK;
+  if (t0 < 0 || t1 < t0 || t1 > nt) return fail(EDKM_E_ARG, "tensor range outside [0, nt]");
+  if (t1 == t0) return EDKM_OK;
   if (!counts || !C0 || !C_out || !table || !saved) return fail(EDKM_E_ARG, "NULL buffer");
   TableArgs P = table_args(nt, p, saved);
   P.counts = counts;
   P.C0 = C0;
   P.C_out = C_out;
   P.table = table;
-  cudaError_t e = P.k >= 32 ? launch_tf_wide(P, (cudaStream_t)stream) : launch_tf(P, (cudaStream_t)stream);
+  const TableArgs R = table_range(P, t0, t1);
+  cudaError_t e = R.k >= 32 ? launch_tf_wide(R, (cudaStream_t)stream) : launch_tf(R, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "TF table-forward launch");
   g_launches = 1;
   return EDKM_OK;
+}
+
+edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
+                         float* table, void* saved, void* stream) {
+  if (nt < 0) {
+    g_launches = 0;
+    return fail(EDKM_E_ARG, "nt < 0");
+  }
+  return edkm_forward_range(counts, nt, 0, nt, p, C0, C_out, table, saved, stream);
 }
 
 edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_params* p, const float* table,
@@ -341,23 +382,53 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
   return st;
 }
 
-edkm_status edkm_backward_table(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
-                                const double* gamma, float* dC0, void* stream) {
+edkm_status edkm_backward_table_range(int nt, int t0, int t1, const edkm_params* p, const int32_t* counts,
+                                      const void* saved, void* ws, const double* gamma, float* dC0, void* stream) {
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
   if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
-  if (nt == 0) return EDKM_OK;
+  if (t0 < 0 || t1 < t0 || t1 > nt) return fail(EDKM_E_ARG, "tensor range outside [0, nt]");
+  if (t1 == t0) return EDKM_OK;
   if (!counts || !saved || !ws || !gamma || !dC0) return fail(EDKM_E_ARG, "NULL buffer");
   TableArgs P = table_args(nt, p, saved);
   ws_args(P, ws);
   P.counts = counts;
   P.gamma = const_cast<double*>(gamma);
   P.dC0 = dC0;
+  const TableArgs R = table_range(P, t0, t1);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = P.k >= 32 ? launch_tb_wide(P, s) : launch_tb(P, s);
+  cudaError_t e = R.k >= 32 ? launch_tb_wide(R, s) : launch_tb(R, s);
   if (e != cudaSuccess) return cuda_fail(e, "TB table-backward launch");
   g_launches = 1;
+  return EDKM_OK;
+}
+
+edkm_status edkm_backward_table(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
+                                const double* gamma, float* dC0, void* stream) {
+  if (nt < 0) {
+    g_launches = 0;
+    return fail(EDKM_E_ARG, "nt < 0");
+  }
+  return edkm_backward_table_range(nt, 0, nt, p, counts, saved, ws, gamma, dC0, stream);
+}
+
+edkm_status edkm_layout(int nt, const edkm_params* p, size_t* saved_offs, size_t* ws_offs) {
+  g_launches = 0;
+  edkm_status st = check_params(p);
+  if (st != EDKM_OK) return st;
+  if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
+  const int k = 1 << p->bits;
+  if (saved_offs) {
+    const SavedLayout L = saved_layout(nt, k, p->max_iter);
+    const size_t v[8] = {L.state, L.ctraj, L.straj, L.rows, L.table16, L.idx8, L.page_cnt, L.total};
+    memcpy(saved_offs, v, sizeof(v));
+  }
+  if (ws_offs) {
+    const WsLayout L = ws_layout(nt, k);
+    const size_t v[5] = {L.B, L.psi, L.phipsi, L.gamma, L.total};
+    memcpy(ws_offs, v, sizeof(v));
+  }
   return EDKM_OK;
 }
 

@@ -45,19 +45,56 @@ def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+def padded_numels(numels, world: int):
+    """Tensor list padded with empty tensors to a multiple of `world` (the table-phase split needs
+    equal per-rank tensor blocks, so that each exchanged array is one all-gather)."""
+    numels = list(numels)
+    return numels + [0] * ((-len(numels)) % world)
+
+
+def allgather_blocks(full: torch.Tensor, group=None):
+    """In-place all-gather of rank blocks: rank r's block is rows [r nt/P, (r+1) nt/P) of `full`."""
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return full
+    P, r = dist.get_world_size(group), dist.get_rank(group)
+    b = full.shape[0] // P
+    dist.all_gather_into_tensor(full, full[r * b:(r + 1) * b].contiguous(), group=group)
+    return full
+
+
 class ShardedStep:
     """Runs one eDKM step over this rank's slices with the two collectives.
 
     `kernels` is any object with the Plan interface (uniquify, forward,
     reconstruct, backward_reduce, backward_apply, counts, gamma, dC0); on a
     B200 it is paper_2309_00964_b200.edkm.Plan.
+
+    shard_table=True splits the table phase by tensor block: rank r runs
+    TF and TB only for tensors [r nt/P, (r+1) nt/P) (edkm_forward_range / _backward_table_range)
+    and the ranks all-gather the per-tensor results the per-weight kernels need -- after TF the
+    tensor state, C trajectory, compacted rows, W~ table(s), page masses and C_T; after TB the
+    (phi, psi) table and dC_0.  Otherwise (default) every rank runs the whole table phase
+    (identical results, no extra exchange).  Requires plan.nt % P == 0 (dist.padded_numels).
+    `out_mode` selects which W~ tables are exchanged: "16" (16-bit soft), "fp32", or "all".
     """
 
-    def __init__(self, kernels, group=None, allreduce=None, nvls=None):
+    def __init__(self, kernels, group=None, allreduce=None, nvls=None, shard_table=False, allgather=None,
+                 out_mode="all"):
         self.k = kernels
         self.group = group
         self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
+        self.allgather = allgather or (lambda t: allgather_blocks(t, self.group))
         self.nvls = nvls
+        self.shard_table = shard_table
+        self.out_mode = out_mode
+
+    def _block(self):
+        P = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        r = dist.get_rank(self.group) if dist.is_initialized() else 0
+        if self.k.nt % P:
+            raise ValueError("shard_table needs plan.nt divisible by the world size (use dist.padded_numels)")
+        b = self.k.nt // P
+        return r * b, (r + 1) * b
 
     def __call__(self, weights, grads, C0, outs, dW):
         if self.nvls is not None:
@@ -65,11 +102,28 @@ class ShardedStep:
         else:
             self.k.uniquify(weights)
             self.allreduce(self.k.counts)                 # exchange 1: integer counts
-        self.k.forward(C0)
+        if not self.shard_table:
+            self.k.forward(C0)
+            self.k.reconstruct(weights, outs)
+            self.k.backward_reduce(weights, grads)
+            self.allreduce(self.k.gamma)                  # exchange 2: gamma_T partials
+            self.k.backward_apply(weights, grads, dW)
+            return self.k.dC0
+        t0, t1 = self._block()
+        v = self.k.views()
+        self.k.forward_range(t0, t1, C0)                  # TF, own tensor block
+        names = ["state", "ctraj", "rows", "page_cnt", "C_out"]
+        names += {"16": ["table16"], "fp32": ["table"]}.get(self.out_mode, ["table16", "table", "idx8"])
+        for n in names:
+            self.allgather(v[n])
         self.k.reconstruct(weights, outs)
-        self.k.backward_reduce(weights, grads)
+        self.k.backward_buckets(weights, grads)
+        self.k.backward_gamma()
         self.allreduce(self.k.gamma)                      # exchange 2: gamma_T partials
-        self.k.backward_apply(weights, grads, dW)
+        self.k.backward_table_range(t0, t1)               # TB, own tensor block
+        for n in ("phipsi", "dC0"):
+            self.allgather(v[n])
+        self.k.backward_dw(weights, grads, dW)
         return self.k.dC0
 
 

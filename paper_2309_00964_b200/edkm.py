@@ -74,6 +74,9 @@ def lib():
             "edkm_uniquify": ([P, i32, i32, P, P], i32),
             "edkm_uniquify_nvls": ([P, i32, i32, ctypes.POINTER(_Nvls), P], i32),
             "edkm_forward": ([P, i32, pp, P, P, P, P, P], i32),
+            "edkm_forward_range": ([P, i32, i32, i32, pp, P, P, P, P, P], i32),
+            "edkm_backward_table_range": ([i32, i32, i32, pp, P, P, P, P, P, P], i32),
+            "edkm_layout": ([i32, pp, P, P], i32),
             "edkm_reconstruct": ([P, i32, pp, P, P, P, i32, i32, P, P], i32),
             "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P], i32),
             "edkm_backward_apply": ([P, i32, pp, P, i32, P, P, P, P, P, i32, P, P], i32),
@@ -104,7 +107,8 @@ def lib():
 
 
 def exported_symbols() -> list:
-    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_uniquify_nvls", "edkm_forward", "edkm_reconstruct",
+    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_uniquify_nvls", "edkm_forward", "edkm_forward_range",
+            "edkm_backward_table_range", "edkm_layout", "edkm_reconstruct",
             "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_backward_buckets",
             "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
             "edkm_last_launch_count", "edkm_set_max_ctas", "edkm_status_string", "edkm_last_error",
@@ -326,6 +330,46 @@ class Plan:
         _check(lib().edkm_forward(_ptr(self.counts), self.nt, ctypes.byref(self.p.c()), _ptr(C0), _ptr(self.C_out),
                                   _ptr(self.table), _ptr(self.saved), _stream(stream)), "edkm_forward")
         return self.C_out
+
+    def forward_range(self, t0, t1, C0, stream=None):
+        """TF for tensors [t0, t1) only (edkm_forward_range)."""
+        _check(lib().edkm_forward_range(_ptr(self.counts), self.nt, t0, t1, ctypes.byref(self.p.c()), _ptr(C0),
+                                        _ptr(self.C_out), _ptr(self.table), _ptr(self.saved), _stream(stream)),
+               "edkm_forward_range")
+        return self.C_out
+
+    def backward_table_range(self, t0, t1, stream=None):
+        """TB for tensors [t0, t1) only (edkm_backward_table_range)."""
+        _check(lib().edkm_backward_table_range(self.nt, t0, t1, ctypes.byref(self.p.c()), _ptr(self.counts),
+                                               _ptr(self.saved), _ptr(self.ws), _ptr(self.gamma), _ptr(self.dC0),
+                                               _stream(stream)), "edkm_backward_table_range")
+        return self.dC0
+
+    SAVED_ARRAYS = ("state", "ctraj", "straj", "rows", "table16", "idx8", "page_cnt")
+    WS_ARRAYS = ("B", "psi", "phipsi", "gamma")
+
+    def views(self):
+        """uint8 views [nt][bytes per tensor] of every per-tensor array of `saved` and `ws` (edkm_layout),
+        plus the C_out / table / dC0 buffers: the blocks ranks exchange when they split the table phase."""
+        if getattr(self, "_views", None) is None:
+            so = (ctypes.c_size_t * 8)()
+            wo = (ctypes.c_size_t * 5)()
+            _check(lib().edkm_layout(self.nt, ctypes.byref(self.p.c()), so, wo), "edkm_layout")
+            nt = max(self.nt, 1)
+            v = {}
+            sizes = {"state": 144, "ctraj": (self.p.max_iter + 1) * self.p.k * 8,
+                     "straj": max(self.p.max_iter, 1) * self.p.k * 8, "rows": PATTERNS * 2, "table16": PATTERNS * 2,
+                     "idx8": PATTERNS, "page_cnt": 256 * 8}
+            for i, name in enumerate(self.SAVED_ARRAYS):
+                v[name] = self.saved[so[i]:so[i] + nt * sizes[name]].view(nt, sizes[name])
+            wsz = {"B": PATTERNS * 8, "psi": PATTERNS * 8, "phipsi": PATTERNS * 8, "gamma": self.p.k * 8}
+            for i, name in enumerate(self.WS_ARRAYS):
+                v[name] = self.ws[wo[i]:wo[i] + nt * wsz[name]].view(nt, wsz[name])
+            for name in ("C_out", "table", "dC0"):
+                t = getattr(self, name)
+                v[name] = t.view(torch.uint8).view(nt, -1)
+            self._views = v
+        return self._views
 
     def reconstruct(self, weights, outs, mode=SOFT, stream=None):
         odt = _DT[outs[0].dtype] if outs else _DT[self.p.wdtype]

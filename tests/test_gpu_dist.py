@@ -31,10 +31,20 @@ def _reduce_via_host(t: torch.Tensor):
     t.copy_(h)
 
 
-def _worker(rank, world, port, q):
+def _gather_via_host(t: torch.Tensor):
+    """all-gather of rank blocks (rows) through host memory (gloo)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    b = t.shape[0] // world
+    parts = [torch.empty_like(t[:b], device="cpu") for _ in range(world)]
+    dist.all_gather(parts, t[rank * b:(rank + 1) * b].cpu())
+    t.copy_(torch.cat(parts).to(t.device))
+
+
+def _worker(rank, world, port, q, shard_table=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_2309_00964_b200.dist import padded_numels
         dev = torch.device("cuda", 0)
         p = E.Params(torch.bfloat16, **P_)
         Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
@@ -42,11 +52,17 @@ def _worker(rank, world, port, q):
         rng = shard_all(SIZES, rank, world)
         Wl = [w[a:b].contiguous().to(dev) for w, (a, b) in zip(Ws, rng)]
         Gl = [g[a:b].contiguous().to(dev) for g, (a, b) in zip(Gs, rng)]
-        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
-        plan = E.Plan([w.numel() for w in Wl], p, dev)
+        numels = [w.numel() for w in Wl]
+        if shard_table:  # empty tensors pad the list to equal per-rank table-phase blocks
+            numels = padded_numels(numels, world)
+            Wl += [torch.empty(0, dtype=torch.bfloat16, device=dev)] * (len(numels) - len(Wl))
+            Gl += [torch.empty(0, dtype=torch.bfloat16, device=dev)] * (len(numels) - len(Gl))
+        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(numels), dtype=torch.float32, device=dev)
+        plan = E.Plan(numels, p, dev)
         outs = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
         dW = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
-        ShardedStep(plan, allreduce=_reduce_via_host)(Wl, Gl, C0, outs, dW)
+        ShardedStep(plan, allreduce=_reduce_via_host, allgather=_gather_via_host, shard_table=shard_table,
+                    out_mode="fp32")(Wl, Gl, C0, outs, dW)
         torch.cuda.synchronize()
         q.put((rank, plan.counts.cpu().numpy(), plan.C_out.cpu().numpy(), plan.dC0.cpu().numpy(),
                [o.cpu().double().numpy() for o in outs], [d.cpu().double().numpy() for d in dW]))
@@ -62,12 +78,15 @@ def free_port():
     return port
 
 
-def test_two_ranks_on_one_gpu_match_single_process_oracle():
+@pytest.mark.parametrize("shard_table", [False, True])
+def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table):
+    """shard_table=True: each rank runs TF/TB for its own tensor block and the ranks all-gather
+    the per-tensor results (SURVEY S8(f) NEXT #2); results must be the same."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shard_table)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = {}
