@@ -211,15 +211,10 @@ class NvlsCounts:
             self.mc_ptrs = [t.data_ptr() for t in self.bufs] + [self.flags.data_ptr()]
             self.current = self.bufs[0][:nt]
             return
+        self._dev = dev
         sup = ctypes.c_int(0)
-        if L.edkm_mc_supported(ctypes.byref(sup)) != 0 or not sup.value:
-            ok = torch.zeros(1, device="cpu")
-        else:
-            ok = torch.ones(1, device="cpu")
-        if self.nranks > 1:
-            ok = self._all_min(ok)
-        if not ok.item():
-            raise NvlsUnavailable("no NVLS multicast support on this system")
+        self._agree(L.edkm_mc_supported(ctypes.byref(sup)) == 0 and bool(sup.value),
+                    "no NVLS multicast support on this system")
         self.nt = max(nt, 1)
         cbytes = (self.nt * 65536 * 4 + 255) // 256 * 256
         need = 2 * cbytes + NVLS_FLAGS * 4
@@ -238,25 +233,29 @@ class NvlsCounts:
             dist.broadcast_object_list(info, src=0, group=group)
         name, size, err = info
         if not size:
-            raise NvlsUnavailable(f"multicast object creation failed: {err}")
-        if self.nranks > 1:
-            if rank == 0:
-                _send_fd(name, fd.value, self.nranks - 1)
-                os.close(fd.value)
-            else:
-                rfd = _recv_fd(name)
-                rc = L.edkm_mc_import(rfd, ctypes.c_size_t(size), ctypes.byref(buf))
-                os.close(rfd)
-                if rc != 0:
-                    raise NvlsUnavailable(f"multicast import failed: {L.edkm_mc_last_error().decode()}")
+            raise NvlsUnavailable(f"multicast object creation failed: {err}")  # identical on every rank
         self._buf = buf
-        if L.edkm_mc_add_device(buf) != 0:
-            raise NvlsUnavailable(f"cuMulticastAddDevice failed: {L.edkm_mc_last_error().decode()}")
-        if self.nranks > 1:
-            dist.barrier(group)
+        ok, why = True, ""
+        if self.nranks > 1:  # rank 0's descriptor to the others (every failure is agreed on below)
+            try:
+                if rank == 0:
+                    _send_fd(name, fd.value, self.nranks - 1)
+                else:
+                    rfd = _recv_fd(name)
+                    rc = L.edkm_mc_import(rfd, ctypes.c_size_t(size), ctypes.byref(buf))
+                    os.close(rfd)
+                    ok, why = rc == 0, f"multicast import failed: {L.edkm_mc_last_error().decode()}"
+            except OSError as e:
+                ok, why = False, f"descriptor hand-off failed: {e}"
+            finally:
+                if rank == 0:
+                    os.close(fd.value)
+        self._agree(ok, why or "descriptor hand-off failed on another rank")
+        rc = L.edkm_mc_add_device(buf)
+        self._agree(rc == 0, f"cuMulticastAddDevice failed: {L.edkm_mc_last_error().decode()}")
         loc, mc = ctypes.c_void_p(), ctypes.c_void_p()
-        if L.edkm_mc_bind(buf, ctypes.byref(loc), ctypes.byref(mc)) != 0:
-            raise NvlsUnavailable(f"multicast bind failed: {L.edkm_mc_last_error().decode()}")
+        rc = L.edkm_mc_bind(buf, ctypes.byref(loc), ctypes.byref(mc))
+        self._agree(rc == 0, f"multicast bind failed: {L.edkm_mc_last_error().decode()}")
         self.local, self.mcbase = loc.value, mc.value
         self.offs = [0, cbytes, 2 * cbytes]
         self.bufs = [torch.as_tensor(_CudaArray(self.local + o, (self.nt, 65536), "<i4"), device=dev)
@@ -270,9 +269,22 @@ class NvlsCounts:
         if self.nranks > 1:
             dist.barrier(group)
 
-    def _all_min(self, t):
-        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
-        return t
+    def _agree(self, ok: bool, why: str):
+        """All ranks learn whether every rank succeeded (MIN all-reduce) and raise together:
+        a rank that gave up alone would leave the others in a collective."""
+        if self.nranks > 1:
+            backend = dist.get_backend(self.group)
+            t = torch.tensor([1.0 if ok else 0.0], device=self._dev if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+            all_ok = bool(t.item() == 1.0)
+        else:
+            all_ok = ok
+        if not all_ok:
+            if getattr(self, "_buf", None) is not None and self._buf.value:
+                from . import edkm as E
+                E.lib().edkm_mc_destroy(self._buf)
+                self._buf = None
+            raise NvlsUnavailable(why if not ok else "failed on another rank")
 
     def next_step(self, stream=None):
         """C struct for this step's call; zeroes the next step's buffer on `stream` first."""

@@ -88,3 +88,42 @@ def test_pipeline_groups_cover_tensors_in_order():
         gs = _groups(numels, g)
         assert sum(gs, []) == list(range(len(numels)))
         assert 1 <= len(gs) <= g and all(gs)
+
+
+def test_range_layout_and_nvls_entry_points_check_arguments(L):
+    """Tensor-range table phase, layout query and the NVLS-fused F1 reject bad arguments before
+    any CUDA call (include/edkm.h conventions)."""
+    p = E.Params()
+    cp = ctypes.byref(p.c())
+    one = ctypes.c_void_p(16)
+    # ranges outside [0, nt] or reversed
+    for t0, t1 in ((-1, 2), (2, 1), (0, 5)):
+        assert L.edkm_forward_range(one, 4, t0, t1, cp, one, one, one, one, None) == 1
+        assert L.edkm_backward_table_range(4, t0, t1, cp, one, one, one, one, one, None) == 1
+    # empty range: nothing to do
+    assert L.edkm_forward_range(one, 4, 2, 2, cp, one, one, one, one, None) == 0
+    assert L.edkm_backward_table_range(4, 3, 3, cp, one, one, one, one, one, None) == 0
+    # layout: offsets increase, the totals match the size queries, arrays hold nt entries each
+    so = (ctypes.c_size_t * 8)()
+    wo = (ctypes.c_size_t * 5)()
+    nt = 7
+    assert L.edkm_layout(nt, cp, so, wo) == 0
+    assert list(so) == sorted(so) and so[7] == L.edkm_saved_bytes(nt, cp)
+    assert list(wo) == sorted(wo) and wo[4] == L.edkm_workspace_bytes(nt, cp)
+    assert so[4] - so[3] >= nt * 65536 * 2 and so[7] - so[6] >= nt * 256 * 8   # rows, page_cnt
+    assert wo[3] - wo[2] >= nt * 65536 * 8                                        # (phi, psi)
+    assert L.edkm_layout(-1, cp, so, wo) == 1
+    # NVLS F1: missing buffers, bad rank count, emulation with several ranks
+    x = E._Nvls(16, 16, 16, 16, 1, 0)
+    assert L.edkm_uniquify_nvls(None, 0, 0, None, None) == 1
+    assert L.edkm_uniquify_nvls(None, 0, 5, ctypes.byref(x), None) == 2
+    assert L.edkm_uniquify_nvls(None, 0, 0, ctypes.byref(E._Nvls(0, 16, 16, 16, 1, 0)), None) == 1
+    assert L.edkm_uniquify_nvls(None, 0, 0, ctypes.byref(E._Nvls(16, 16, 16, 16, 0, 0)), None) == 1
+    assert L.edkm_uniquify_nvls(None, 0, 0, ctypes.byref(E._Nvls(16, 16, 16, 16, 2, 1)), None) == 1
+    # multicast plumbing
+    assert L.edkm_mc_create(0, 1, 0, None, None) == 1
+    assert L.edkm_mc_import(-1, 1 << 21, None) == 1
+    assert L.edkm_mc_add_device(None) == 1
+    assert L.edkm_mc_bytes(None) == 0
+    assert L.edkm_mc_destroy(None) == 0
+    assert L.edkm_set_max_ctas(0) == 0 and L.edkm_set_max_ctas(3) == 0 and L.edkm_set_max_ctas(0) == 3
