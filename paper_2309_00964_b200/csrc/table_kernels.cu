@@ -29,7 +29,10 @@ namespace cg = cooperative_groups;
 
 namespace edkm {
 
-constexpr int kFThreads = 256;  // TF, TGAMMA: small shared footprint, two CTAs per SM
+#ifndef EDKM_FTHREADS
+#define EDKM_FTHREADS 256
+#endif
+constexpr int kFThreads = EDKM_FTHREADS;  // TF, TGAMMA: small shared footprint, two CTAs per SM
 constexpr int kBThreads = 512;  // TB: 192 KiB of staged rows, one CTA per SM
 constexpr int kStage = 12288;  // rows per CTA staged in shared memory: value (f32), count (i32), psi (f64)
 constexpr size_t kStageBytesF = (size_t)kStage * 8;   // TF: value + count
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
     if (sign_split) {  // one signed page = 256 patterns = 16 threads (the ranges are page-aligned)
 #pragma unroll
       for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
-      if ((lane & 15) == 0) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
+      if ((lane & 15) == 0 && in) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
     }
     if (in) {
       // NaN fill (populated entries are overwritten in phase 3); hard index 0 for non-finite patterns
