@@ -263,6 +263,60 @@ __device__ __forceinline__ void fixed_carry(uint32_t saddr, int q, uint32_t old)
       ::"r"(saddr), "r"(old), "r"(q), "n"(HI_OFF));
 }
 
+// ---------------------------------------------------------------- TMA staging of per-pattern tables
+// The per-segment tables (W~ table, index table, (phi, psi) window) are copied global -> shared
+// by the bulk-copy engine (cp.async.bulk, completion counted in bytes on an mbarrier) instead of
+// by the 1024 threads: one elected thread issues the copies, every thread waits on the phase.
+struct TmaTable {
+  uint64_t* bar;   // shared mbarrier (arrival count 1)
+  uint32_t phase;  // parity of the next completion (uniform across the CTA)
+  // called by every thread once per kernel, before the first stage()
+  __device__ void init(uint64_t* b) {
+    bar = b;
+    phase = 0;
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  // Copy up to two contiguous global ranges into shared memory (bytes multiples of 16, both
+  // addresses 16-byte aligned; the caller checks and otherwise uses plain loads) and wait.
+  // Must be entered by every thread after a barrier that ended all reads of `dst0`/`dst1`.
+  __device__ void stage(void* dst0, const void* src0, uint32_t bytes0, void* dst1 = nullptr,
+                        const void* src1 = nullptr, uint32_t bytes1 = 0) {
+    if (threadIdx.x == 0) {
+      // the generic-proxy reads of the previous segment's table precede these async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                   "r"(bytes0 + bytes1)
+                   : "memory");
+      copy(dst0, src0, bytes0);
+      if (bytes1) copy(dst1, src1, bytes1);
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TMA_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TMA_WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+  }
+  __device__ void copy(void* dst, const void* src, uint32_t bytes) {
+    constexpr uint32_t kPiece = 32768;
+    for (uint32_t o = 0; o < bytes; o += kPiece) {
+      const uint32_t n = bytes - o < kPiece ? bytes - o : kPiece;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(dst) + o),
+                   "l"((const char*)src + o), "r"(n), "r"(smem_addr(bar))
+                   : "memory");
+    }
+  }
+  static __device__ __forceinline__ bool aligned(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+};
+
 // (phi, psi) of a pattern: shared window when `in` != 0, else the global table
 // entry gtab[u] (its address is formed inside the predicated block).
 __device__ __forceinline__ float2 lookup_f2(uint32_t in, uint32_t saddr, const float2* gtab, uint32_t u) {

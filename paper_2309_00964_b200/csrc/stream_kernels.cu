@@ -149,8 +149,14 @@ struct F1Policy {
 // (fp16, whose pages are quarter binades, or unusual data) takes the shared-array path.
 constexpr int kF1LPages = 7;
 constexpr int kF1LRows = kF1LPages * 256;  // 1792 words per copy, 32 copies = 224 KiB
-constexpr int kF1LChunkVec = 127;          // vectors per thread between folds (32*127*16 < 65536)
+// vectors per thread between folds (32*127*16 < 65536); measured: 4x fewer folds would save
+// only ~3% of F1, not worth an unsafe bound
+constexpr int kF1LChunkVec = 127;
 constexpr int kF1Sample = 16384;
+// dynamic shared memory of F1: the shared-array path's counters, or the lane-private copies
+// plus one trash row (never folded) that absorbs the increments of patterns outside the window
+constexpr size_t kF1Smem = (size_t)(kF1LRows + 1) * 128 > (size_t)kF1Bins * 4
+                               ? (size_t)(kF1LRows + 1) * 128 : (size_t)kF1Bins * 4;
 
 template <int MC>
 __device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u) { cnt_add<MC>(&c[u], 1); }
@@ -276,41 +282,38 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
       const int64_t nv = (b - va) >> 4;
       for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global<MC>(cnt, w[i]);
       for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global<MC>(cnt, w[i]);
-      // one 16-pattern vector: lane-private increments, or per element when it leaves the window
+      // one 16-pattern vector.  Every lane takes the same straight-line path: a pattern outside
+      // the window is clamped to the trash row kF1LRows (never folded), and the lanes holding
+      // such a pattern (~0.1% of bf16 N(0, 0.02^2) weights, but ~40% of warp iterations see one)
+      // then add it to the global count in a short pass.  Before, a whole per-element slow path
+      // ran divergently for those lanes (ncu: 26.9 of 32 threads active per warp).
+      const uint32_t lim2 = (uint32_t)kF1LRows * 0x10001u;
       auto count_vec = [&](const V8& r) {
-        uint32_t rel[8], rmax2 = 0;
+        uint32_t rmax2 = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          rel[q] = __vadd2(r.x[q] & 0x7FFF7FFFu, pb2);
-          rmax2 = __vmaxu2(rmax2, rel[q]);
+          const uint32_t x = r.x[q];
+          const uint32_t rel = __vadd2(x & 0x7FFF7FFFu, pb2);
+          rmax2 = __vmaxu2(rmax2, rel);
+          const uint32_t rc = __vminu2(rel, lim2);
+          // row offsets by IMAD (k16, k128 are kernel parameters, opaque to ptxas, so the
+          // multiplies stay on the FMA pipe); the increment 1 or 0x10000 (the sign selects the
+          // counter half) from one PRMT sign-replicate + 1.  F1 is ALU-pipe bound otherwise.
+          const uint32_t rh = __umulhi(rc, k16);
+          const uint32_t rl = rc & 0xFFFFu;
+          uint32_t mlo, mhi;
+          asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));
+          asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));
+          red_add_shared(rl * k128 + base, mlo + 1u);
+          red_add_shared(rh * k128 + base, mhi + 1u);
         }
-        if (max(rmax2 & 0xFFFFu, rmax2 >> 16) < (uint32_t)kF1LRows) {
-          // Per 16-bit pair: row offsets by IMAD (k16, k128 are kernel parameters, opaque to
-          // ptxas, so the multiplies stay on the FMA pipe); the increment 1 or 0x10000 (sign of
-          // the pattern selects the counter half) from one PRMT sign-replicate + 1.  F1 is
-          // ALU-pipe bound otherwise (ncu: ALU 83%, FMA-heavy 34%).
+        if (max(rmax2 & 0xFFFFu, rmax2 >> 16) >= (uint32_t)kF1LRows) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const uint32_t x = r.x[q];
-            const uint32_t rh = __umulhi(rel[q], k16);
-            const uint32_t rl = rel[q] & 0xFFFFu;
-            uint32_t mlo, mhi;
-            asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));  // 0xFFFF if bit 15 set
-            asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));  // 0xFFFF if bit 31 set
-            red_add_shared(rl * k128 + base, mlo + 1u);
-            red_add_shared(rh * k128 + base, mhi + 1u);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint32_t x = r.x[q];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint32_t rr = e ? (rel[q] >> 16) : (rel[q] & 0xFFFFu);
-              const uint32_t u = e ? (x >> 16) : (x & 0xFFFFu);
-              if (rr < (uint32_t)kF1LRows) red_add_shared(base + (rr << 7), 1u + (u >> 15) * 0xFFFFu);
-              else f1_count_global<MC>(cnt, u);
-            }
+            const uint32_t rel = __vadd2(x & 0x7FFF7FFFu, pb2);
+            if ((rel & 0xFFFFu) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x & 0xFFFFu);
+            if ((rel >> 16) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x >> 16);
           }
         }
       };
@@ -379,15 +382,22 @@ struct F2Policy {
   const StreamArgs& A;
   const F2Args& F;
   unsigned char* sm;
+  TmaTable tma;
   int pbase, np;
   struct Vec { V8 w; };
   __device__ int gt(int t) const { return A.t0 + t; }
   __device__ void begin(int t, int64_t, int64_t) {
     const int T = gt(t);
     if (MODE == 0) {
-      const uint4* src = reinterpret_cast<const uint4*>(F.table16 + (int64_t)T * kPatterns);
+      // the whole 16-bit W~ table (128 KiB), staged by TMA
+      const uint16_t* src = F.table16 + (int64_t)T * kPatterns;
+      if (TmaTable::aligned(src)) {
+        tma.stage(sm, src, kPatterns * 2);
+        return;
+      }
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
       uint4* dst = reinterpret_cast<uint4*>(sm);
-      for (int i = threadIdx.x; i < kPatterns * 2 / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+      for (int i = threadIdx.x; i < kPatterns * 2 / 16; i += blockDim.x) dst[i] = __ldg(s4 + i);
     } else if (MODE == 1) {
       uint16_t* tab = reinterpret_cast<uint16_t*>(sm);
       const uint8_t* ix = F.idx8 + (int64_t)T * kPatterns;
@@ -402,16 +412,28 @@ struct F2Policy {
       np = s_w[1];
       float* tab = reinterpret_cast<float*>(sm);
       const float* src = F.table + (int64_t)T * kPatterns;
+      if (TmaTable::aligned(src)) {
+        // the window's two halves are contiguous ranges of the table: patterns pbase*256.. of each sign
+        const uint32_t half = (uint32_t)np * 256u;
+        tma.stage(tab, src + pbase * 256, half * 4, tab + half, src + 0x8000 + pbase * 256, half * 4);
+        return;
+      }
       for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
     } else {
       uint8_t* ix = reinterpret_cast<uint8_t*>(sm);
-      const uint4* src = reinterpret_cast<const uint4*>(F.idx8 + (int64_t)T * kPatterns);
-      uint4* dst = reinterpret_cast<uint4*>(ix);
-      for (int i = threadIdx.x; i < kPatterns / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-      if (MODE == 3) {
+      const uint8_t* src = F.idx8 + (int64_t)T * kPatterns;
+      if (MODE == 3) {  // the centroids, next to the index table (end() of the last segment synced)
         float* Cs = reinterpret_cast<float*>(sm + kPatterns);
         if (threadIdx.x < F.k) Cs[threadIdx.x] = F.C[(int64_t)T * F.k + threadIdx.x];
       }
+      if (TmaTable::aligned(src)) {
+        tma.stage(ix, src, kPatterns);
+        if (MODE == 3) __syncthreads();  // Cs
+        return;
+      }
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* dst = reinterpret_cast<uint4*>(ix);
+      for (int i = threadIdx.x; i < kPatterns / 16; i += blockDim.x) dst[i] = __ldg(s4 + i);
     }
     __syncthreads();
   }
@@ -468,8 +490,10 @@ struct F2Policy {
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_constant__ StreamArgs A, const F2Args F) {
-  extern __shared__ __align__(16) unsigned char smem_u8[];
-  F2Policy<MODE> p{A, F, smem_u8, 0, 0};
+  extern __shared__ __align__(128) unsigned char smem_u8[];
+  __shared__ uint64_t s_bar;
+  F2Policy<MODE> p{A, F, smem_u8, {}, 0, 0};
+  p.tma.init(&s_bar);
   for_each_segment(A, p);
 }
 
@@ -689,6 +713,7 @@ struct B2Policy {
   const StreamArgs& A;
   const B2Args& Bq;
   float2* tab;
+  TmaTable tma;
   int pbase, np;
   uint32_t negpb2;  // -pbase*256 in both 16-bit halves
   Win win;
@@ -706,9 +731,15 @@ struct B2Policy {
     pbase = s_w[0];
     np = s_w[1];
     const float2* src = glob(t);
-    for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
     win.init<8>(smem_addr(tab), pbase, np);
     negpb2 = ((0x10000u - win.pb256) & 0xFFFFu) * 0x10001u;
+    if (TmaTable::aligned(src)) {
+      // the window's two halves are contiguous ranges of the (phi, psi) table, staged by TMA
+      const uint32_t half = (uint32_t)np * 256u;
+      tma.stage(tab, src + pbase * 256, half * 8, tab + half, src + 0x8000 + pbase * 256, half * 8);
+      return;
+    }
+    for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) tab[s] = __ldg(src + slot_pattern(s, pbase, np));
     __syncthreads();
   }
   __device__ bool vec_ok(int t, int64_t i) const {
@@ -797,8 +828,10 @@ struct B2Policy {
 
 template <int GDT, int ODT>
 __global__ void __launch_bounds__(kThreads, 1) b2_dw_kernel(const __grid_constant__ StreamArgs A, const B2Args Bq) {
-  extern __shared__ __align__(16) float2 smem_b2[];
-  B2Policy<GDT, ODT> p{A, Bq, smem_b2};
+  extern __shared__ __align__(128) float2 smem_b2[];
+  __shared__ uint64_t s_bar;
+  B2Policy<GDT, ODT> p{A, Bq, smem_b2, {}};
+  p.tma.init(&s_bar);
   for_each_segment(A, p);
 }
 
@@ -815,7 +848,7 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s) {
   if (A.total == 0) return cudaSuccess;
-  const size_t smem = kF1Bins * sizeof(uint32_t);
+  const size_t smem = kF1Smem;
   cudaError_t e = set_smem((const void*)f1_hist_kernel<0>, smem);
   if (e != cudaSuccess) return e;
   f1_hist_kernel<0><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, 0x10000u, 128u, nullptr);
@@ -826,7 +859,7 @@ cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_
 // signalling its arrival counter; then the wait kernel.
 cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
                            uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s) {
-  const size_t smem = kF1Bins * sizeof(uint32_t);
+  const size_t smem = kF1Smem;
   const void* fn = emulate ? (const void*)f1_hist_kernel<2> : (const void*)f1_hist_kernel<1>;
   cudaError_t e = set_smem(fn, smem);
   if (e != cudaSuccess) return e;
