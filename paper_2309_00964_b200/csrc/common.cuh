@@ -108,6 +108,57 @@ __device__ __forceinline__ int find_tensor(const StreamArgs& A, int64_t e) {
   return lo;
 }
 
+// Warp-parallel choice of the `cap` consecutive magnitude pages (of kMagPages = 128) with the
+// largest total mass: lane l holds the masses of pages l, l+32, l+64, l+96 in m[0..3].  Returns
+// (in every lane) the smallest start b maximising sum(mass[b .. b+cap)) and that sum in `best`
+// -- the same window as a serial sliding-window scan that keeps the first maximum.  Called by
+// one full warp; replaces a 128-step loop on one lane (~3 us of shared-memory latency per
+// segment, paid by every per-weight kernel).
+template <class T>
+__device__ __forceinline__ int warp_best_window(const T (&m)[4], int cap, T& best) {
+  const int lane = threadIdx.x & 31;
+  // prefix sums in page order: page p = lane + 32 q; exclusive prefix over all pages
+  T pre[4];  // mass of pages < lane + 32 q
+  T carry = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    T inc = m[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    pre[q] = carry + inc - m[q];
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  // window starting at page b = lane + 32 q: prefix(b + cap) - prefix(b); prefix(128) = carry
+  T bw = -1;
+  int bs = 1 << 30;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int b = lane + 32 * q, e = b + cap;  // prefix(e) lives in lane e % 32, slot e / 32
+    T pe = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const T x = __shfl_sync(0xffffffffu, pre[r], e & 31);
+      if ((e >> 5) == r) pe = x;
+    }
+    if (e == kMagPages) pe = carry;
+    if (e <= kMagPages) {
+      const T w = pe - pre[q];
+      if (w > bw) { bw = w; bs = b; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const T ow = __shfl_xor_sync(0xffffffffu, bw, o);
+    const int ob = __shfl_xor_sync(0xffffffffu, bs, o);
+    if (ow > bw || (ow == bw && ob < bs)) { bw = ow; bs = ob; }
+  }
+  best = bw;
+  return bs;
+}
+
 // ---------------------------------------------------------------- magnitude-page window
 // page_cnt[256] (int64, weights per signed page u>>8, every present pattern) is
 // written by the forward table kernel.  Choose np <= cap consecutive magnitude
@@ -136,20 +187,10 @@ __device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, 
     if (lane == 0) { *out_base = pmin; *out_np = pmax - pmin + 1; *out_covers = 1; }
     return;
   }
-  // sliding window of `cap` pages maximising the mass (lane 0, 128 steps)
-  __shared__ int64_t s_mass[kMagPages];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) s_mass[lane + 32 * q] = m[q];
-  __syncwarp();
+  // the `cap` consecutive pages with the most mass (warp-parallel, the first such window)
+  int64_t best;
+  const int bb = warp_best_window(m, cap, best);
   if (lane == 0) {
-    int64_t cur = 0;
-    for (int p = 0; p < cap; ++p) cur += s_mass[p];
-    int64_t best = cur;
-    int bb = 0;
-    for (int p = cap; p < kMagPages; ++p) {
-      cur += s_mass[p] - s_mass[p - cap];
-      if (cur > best) { best = cur; bb = p - cap + 1; }
-    }
     *out_base = bb;
     *out_np = cap;
     *out_covers = 0;

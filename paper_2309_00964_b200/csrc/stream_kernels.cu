@@ -184,6 +184,41 @@ __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
   }
 }
 
+// F1's window: the kF1LPages consecutive magnitude pages holding most of a 16K-pattern sample of
+// the segment [a, b), and whether the lane-private path pays (every thread calls it; the result
+// is in *s_base / *s_lp after the closing barrier).
+__device__ __forceinline__ void f1_choose_window(const uint16_t* w, int64_t a, int64_t b, int wdtype, uint32_t* s_pg,
+                                              int* s_base, int* s_lp) {
+  const int tid = threadIdx.x;
+  if (tid < kMagPages) s_pg[tid] = 0;
+  __syncthreads();
+  if (wdtype == kBF16) {
+    // (a vectorised sample with a warp-aggregated add measured 6% slower overall: its registers
+    // changed the allocation of the hot loop)
+    const int64_t se = min(b, a + kF1Sample);
+#pragma unroll 4
+    for (int64_t i = a + tid; i < se; i += blockDim.x) atomicAdd(&s_pg[(w[i] >> 8) & 0x7F], 1u);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    long long m[4], tot = 0, best;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      m[q] = s_pg[tid + 32 * q];
+      tot += m[q];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const int bb = warp_best_window(m, kF1LPages, best);
+    if (tid == 0) {
+      *s_base = bb;
+      // lane-private path when the window holds >= 98% of a non-trivial sample
+      *s_lp = wdtype == kBF16 && tot >= 1024 && best * 50 >= tot * 49;
+    }
+  }
+  __syncthreads();
+}
+
 template <int MC>
 __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, uint32_t k16, uint32_t k128);
 
@@ -246,27 +281,7 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
     const uint16_t* w = A.w[t];
     int32_t* cnt = counts + (int64_t)(A.t0 + t) * kPatterns;
     // ---- choose the lane-private window from a sample of the segment
-    if (tid < kMagPages) s_pg[tid] = 0;
-    __syncthreads();
-    const int64_t se = min(b, a + kF1Sample);
-    if (A.wdtype == kBF16)
-      for (int64_t i = a + tid; i < se; i += bs) atomicAdd(&s_pg[(w[i] >> 8) & 0x7F], 1u);
-    __syncthreads();
-    if (tid == 0) {
-      // the kF1LPages consecutive magnitude pages holding most of the sample
-      uint32_t tot = 0, cur = 0, best = 0, bb = 0;
-      for (int p = 0; p < kMagPages; ++p) tot += s_pg[p];
-      for (int p = 0; p < kF1LPages; ++p) cur += s_pg[p];
-      best = cur;
-      for (int p = kF1LPages; p < kMagPages; ++p) {
-        cur += s_pg[p] - s_pg[p - kF1LPages];
-        if (cur > best) { best = cur; bb = p - kF1LPages + 1; }
-      }
-      s_base = (int)bb;
-      // lane-private path when the window holds >= 98% of a non-trivial sample
-      s_lp = A.wdtype == kBF16 && tot >= 1024 && (uint64_t)best * 50 >= (uint64_t)tot * 49;
-    }
-    __syncthreads();
+    f1_choose_window(w, a, b, A.wdtype, s_pg, &s_base, &s_lp);
     if (s_lp) {
       const uint32_t pb2 = ((0x10000u - ((uint32_t)s_base << 8)) & 0xFFFFu) * 0x10001u;  // -pbase*256, both halves
       const uint32_t base = smem_addr(h) + (uint32_t)lane * 4u;
