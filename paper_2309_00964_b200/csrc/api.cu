@@ -300,7 +300,7 @@ edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_para
   F.table16 = reinterpret_cast<const uint16_t*>(b + L.table16);
   F.idx8 = b + L.idx8;
   F.C = C_out;
-  F.page_cnt = reinterpret_cast<const int64_t*>(b + L.page_cnt);
+  F.state = reinterpret_cast<const TensorState*>(b + L.state);
   F.k = k;
   static thread_local StreamArgs A;
   A.wdtype = p->wdtype;
@@ -339,7 +339,7 @@ edkm_status edkm_backward_buckets(const edkm_tensor* tensors, int nt, const edkm
   if (e != cudaSuccess) return cuda_fail(e, "memset buckets");
   B1Args Bq;
   Bq.B = const_cast<double*>(P.B);
-  Bq.page_cnt = P.page_cnt;
+  Bq.state = P.state;
   static thread_local StreamArgs A;
   A.wdtype = p->wdtype;
   A.gdtype = gdtype;
@@ -447,7 +447,7 @@ edkm_status edkm_backward_dw(const edkm_tensor* tensors, int nt, const edkm_para
   ws_args(P, const_cast<void*>(ws));
   B2Args Bq;
   Bq.phipsi = P.phipsi;
-  Bq.page_cnt = P.page_cnt;
+  Bq.state = P.state;
   static thread_local StreamArgs A;
   A.wdtype = p->wdtype;
   A.gdtype = gdtype;

@@ -160,13 +160,15 @@ __device__ __forceinline__ int warp_best_window(const T (&m)[4], int cap, T& bes
 }
 
 // ---------------------------------------------------------------- magnitude-page window
-// page_cnt[256] (int64, weights per signed page u>>8, every present pattern) is
-// written by the forward table kernel.  Choose np <= cap consecutive magnitude
-// pages [pbase, pbase+np) that hold the most weights; *out_covers = 1 when the
-// window holds every present pattern (the per-weight kernels then take their
-// fast path with no per-element range check).  Called by one warp.
-__device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, int* out_base, int* out_np,
-                                              int* out_covers) {
+// page_cnt[256] (int64, weights per signed page u>>8, every present pattern) is written by the
+// forward table kernel, which then chooses, once per tensor, the np <= cap consecutive
+// magnitude pages [pbase, pbase+np) that the per-weight kernels keep in shared memory (both
+// signs); patterns outside take a slower path.  Called by one full warp; every lane gets the
+// result.  The window is the whole populated span when it fits in cap pages; otherwise the
+// narrowest window that still holds all but ~1e-6 of the weights (a 16-vector with a pattern
+// outside it takes the slow path, so that tail must be rare, while every page kept costs
+// shared-memory set-up, staging and flushing in each segment of each per-weight kernel).
+__device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, int& pbase, int& np) {
   const int lane = threadIdx.x & 31;
   // masses of magnitude pages lane, lane+32, lane+64, lane+96
   int64_t m[4];
@@ -182,20 +184,21 @@ __device__ __forceinline__ void choose_window(const int64_t* page_cnt, int cap, 
     pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
     pmax = max(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
   }
-  if (pmax < 0) { if (lane == 0) { *out_base = 0; *out_np = 1; *out_covers = 0; } return; }  // keep np >= 1
-  if (pmax - pmin + 1 <= cap) {
-    if (lane == 0) { *out_base = pmin; *out_np = pmax - pmin + 1; *out_covers = 1; }
-    return;
-  }
-  // the `cap` consecutive pages with the most mass (warp-parallel, the first such window)
+  if (pmax < 0) { pbase = 0; np = 1; return; }  // keep np >= 1
+  if (pmax - pmin + 1 <= cap) { pbase = pmin; np = pmax - pmin + 1; return; }
+  int64_t tot = m[0] + m[1] + m[2] + m[3];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  const int64_t need = tot - (tot >> 20);
   int64_t best;
-  const int bb = warp_best_window(m, cap, best);
-  if (lane == 0) {
-    *out_base = bb;
-    *out_np = cap;
-    *out_covers = 0;
+  int lo = 1, hi = cap;  // smallest width whose best window reaches `need` (cap if none)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    warp_best_window(m, mid, best);
+    if (best >= need) hi = mid; else lo = mid + 1;
   }
-  __syncwarp();
+  pbase = warp_best_window(m, lo, best);
+  np = lo;
 }
 
 // slot of pattern u in a window, or -1

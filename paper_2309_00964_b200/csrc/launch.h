@@ -9,12 +9,15 @@ namespace edkm {
 
 // ---- per-tensor forward state kept in `saved`
 constexpr int kMaxCluster = 8;
+constexpr int kWinPagesB = 55;    // magnitude pages per sign kept in shared memory by B1 (8 B/pattern) and B2 (float2)
+constexpr int kWinPagesF2 = 110;  // F2 with fp32 output (4 B/pattern)
 struct TensorState {
   int32_t T;                       // centroid updates run
   int32_t cl;                      // CTAs per tensor in the table phase (row partitions)
   int32_t pbase[kMaxCluster + 1];  // partition p = patterns [pbase[p], pbase[p+1]) (16-aligned, row-balanced)
   int32_t nrows[kMaxCluster];      // populated finite patterns, per partition (stored at rows[pbase[p]...])
-  int32_t pad0;
+  uint8_t win[4];                  // magnitude-page windows of the per-weight kernels (TF, once per
+                                   // tensor): B1/B2 (pbase, np), F2 fp32 output (pbase, np)
   int64_t nonfinite[kMaxCluster];  // NaN/Inf weights counted, per partition
 };
 static_assert(sizeof(TensorState) == 144, "TensorState layout");
@@ -34,16 +37,16 @@ struct F2Args {
   const uint16_t* table16;  // [nt][65536] W~ rounded to the weights' dtype
   const uint8_t* idx8;      // [nt][65536] hard index per pattern
   const float* C;           // [nt][k] C_out
-  const int64_t* page_cnt;  // [nt][256]
+  const TensorState* state; // [nt]: the magnitude-page windows
   int k;
 };
 struct B1Args {
   double* B;                // [nt][65536] fp64, zeroed by the caller
-  const int64_t* page_cnt;  // [nt][256]
+  const TensorState* state; // [nt]: the magnitude-page windows
 };
 struct B2Args {
   const float2* phipsi;     // [nt][65536] (phi, psi) per pattern
-  const int64_t* page_cnt;  // [nt][256]
+  const TensorState* state; // [nt]: the magnitude-page windows
 };
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s);
 cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,

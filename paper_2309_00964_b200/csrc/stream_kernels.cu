@@ -20,9 +20,9 @@ namespace edkm {
 constexpr int kThreads = 1024;   // F1, F2
 
 constexpr int kF1Bins = 57344;  // patterns < 0xE000 counted in SMEM (224 KiB); the rest in L2
-constexpr int kB1Pages = 55;    // magnitude pages per sign kept by B1 (8 B/pattern)
-constexpr int kB2Pages = 55;    // B2 (float2 phi, psi)
-constexpr int kF2Pages32 = 110; // F2 fp32 output (4 B/pattern)
+constexpr int kB1Pages = kWinPagesB;    // magnitude pages per sign kept by B1 (8 B/pattern)
+constexpr int kB2Pages = kWinPagesB;    // B2 (float2 phi, psi)
+constexpr int kF2Pages32 = kWinPagesF2; // F2 fp32 output (4 B/pattern)
 
 // ----------------------------------------------------------------------------
 // Generic visitor over this CTA's slice of the concatenated tensors.
@@ -420,11 +420,8 @@ struct F2Policy {
       for (int u = threadIdx.x; u < kPatterns; u += blockDim.x)
         tab[u] = pattern_finite(u, A.wdtype) ? round16f(__ldg(C + ix[u]), A.wdtype) : nan16(A.wdtype);
     } else if (MODE == 2) {
-      __shared__ int s_w[3];
-      if (threadIdx.x < 32) choose_window(F.page_cnt + (int64_t)T * 256, kF2Pages32, &s_w[0], &s_w[1], &s_w[2]);
-      __syncthreads();
-      pbase = s_w[0];
-      np = s_w[1];
+      pbase = F.state[T].win[2];  // chosen once per tensor by TF (table_windows)
+      np = F.state[T].win[3];
       float* tab = reinterpret_cast<float*>(sm);
       const float* src = F.table + (int64_t)T * kPatterns;
       if (TmaTable::aligned(src)) {
@@ -560,18 +557,15 @@ struct B1Policy {
     return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], GDT);
   }
   __device__ void begin(int t, int64_t a, int64_t b) {
-    __shared__ int s_w[3];
     __shared__ unsigned s_max;
     if (threadIdx.x == 0) s_max = 0;
-    if (threadIdx.x < 32)
-      choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB1Pages, &s_w[0], &s_w[1], &s_w[2]);
-    __syncthreads();
-    pbase = s_w[0];
-    np = s_w[1];
+    pbase = Bq.state[A.t0 + t].win[0];  // chosen once per tensor by TF (table_windows)
+    np = Bq.state[A.t0 + t].win[1];
     uint4* z = reinterpret_cast<uint4*>(lo);
     for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) z[s] = make_uint4(kLoBias, kLoBias, kLoBias, kLoBias);
     uint4* zh = reinterpret_cast<uint4*>(hi);
     for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) zh[s] = make_uint4(0, 0, 0, 0);
+    __syncthreads();  // s_max = 0 before any atomicMax
     // scale from the max finite |G| of a sample (whole segment if the sample is all zero)
     unsigned m = 0;
     const int64_t sample_end = min(b, a + 16384);
@@ -739,12 +733,8 @@ struct B2Policy {
     return decode16f(reinterpret_cast<const uint16_t*>(A.g[t])[i], GDT);
   }
   __device__ void begin(int t, int64_t, int64_t) {
-    __shared__ int s_w[3];
-    if (threadIdx.x < 32)
-      choose_window(Bq.page_cnt + (int64_t)(A.t0 + t) * 256, kB2Pages, &s_w[0], &s_w[1], &s_w[2]);
-    __syncthreads();
-    pbase = s_w[0];
-    np = s_w[1];
+    pbase = Bq.state[A.t0 + t].win[0];  // chosen once per tensor by TF (table_windows)
+    np = Bq.state[A.t0 + t].win[1];
     const float2* src = glob(t);
     win.init<8>(smem_addr(tab), pbase, np);
     negpb2 = ((0x10000u - win.pb256) & 0xFFFFu) * 0x10001u;

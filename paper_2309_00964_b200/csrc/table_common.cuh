@@ -112,4 +112,19 @@ __device__ void table_partitions(const int32_t* cnt, int wdtype, int64_t* page_c
   __syncthreads();
 }
 
+// End of TF: once every CTA of the cluster has written its page masses (call after a cluster
+// barrier), CTA 0's first warp chooses the magnitude-page windows of the per-weight kernels for
+// this tensor and stores them in its TensorState (B1/B2, and F2 with fp32 output), so no
+// per-weight kernel searches for them per segment.
+__device__ __forceinline__ void table_windows(const int64_t* page_cnt, TensorState* st, int crank) {
+  const int warp = threadIdx.x >> 5;
+  if (crank != 0 || warp > 1) return;
+  int pb, np;  // warp 0: the B1/B2 window, warp 1: the F2 fp32 window (in parallel)
+  choose_window(page_cnt, warp == 0 ? kWinPagesB : kWinPagesF2, pb, np);
+  if ((threadIdx.x & 31) == 0) {
+    st->win[2 * warp] = (uint8_t)pb;
+    st->win[2 * warp + 1] = (uint8_t)np;
+  }
+}
+
 }  // namespace edkm

@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
     tab[u] = (float)wt;
     tab16[u] = round16(wt, P.wdtype);
   }
-  cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it
+  cluster.sync();  // keep this CTA's shared memory alive until the cluster is done with it; page masses complete
+  table_windows(P.page_cnt + (int64_t)t * 256, st, crank);
 }
 
 // ============================================================================ TGAMMA

@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
       tab16[u] = round16(wt, P.wdtype);
     }
   }
-  cluster.sync();
+  cluster.sync();  // page masses complete
+  table_windows(P.page_cnt + (int64_t)t * 256, P.state + t, crank);
 }
 
 // ============================================================================ TGAMMA (wide)
