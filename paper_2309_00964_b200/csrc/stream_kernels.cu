@@ -141,7 +141,7 @@ struct F1Policy {
 // lies entirely in its own bank (word = row * 32 + lane), so a warp's 32 atomics always hit 32
 // distinct banks: one wavefront per instruction.  32 copies fit for a window of kF1LPages
 // magnitude pages: word `row` = rel of a pattern (u & 0x7FFF) - pbase*256 holds the 16-bit
-// counters of both signs (positive in the low half).  A copy is shared by the 32 threads with
+// counters of both signs (word = P + 0xFF01 * N, see kF1NegInc).  A copy is shared by the 32 threads with
 // the same lane id, so after 32 x kF1LChunkVec x 16 < 65536 increments the copies are folded
 // into per-thread 32-bit accumulators (each thread owns rows tid and tid + 1024) and zeroed.
 // The window is chosen per segment from a sample; bf16 N(0, 0.02^2) keeps ~99.9% of the weights
@@ -153,6 +153,11 @@ constexpr int kF1LRows = kF1LPages * 256;  // 1792 words per copy, 32 copies = 2
 // only ~3% of F1, not worth an unsafe bound
 constexpr int kF1LChunkVec = 127;
 constexpr int kF1Sample = 16384;
+// Lane-private counter word = P + kF1NegInc * N (P, N: counts of the positive and negative
+// pattern of the row since the last fold, P + N <= 32 * kF1LChunkVec * 16 = 65024 < kF1NegInc,
+// so the word is < 2^32 and decodes exactly).  The increment 1 or 0xFF01 is one PRMT.
+constexpr uint32_t kF1NegInc = 0xFF01u;
+static_assert(32u * kF1LChunkVec * 16u < kF1NegInc, "F1 lane-private counter decoding");
 // dynamic shared memory of F1: the shared-array path's counters, or the lane-private copies
 // plus one trash row (never folded) that absorbs the increments of patterns outside the window
 constexpr size_t kF1Smem = (size_t)(kF1LRows + 1) * 128 > (size_t)kF1Bins * 4
@@ -174,8 +179,10 @@ __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
       for (int s = 0; s < 8; ++s) {
         const int q = (tid + s) & 7;  // diagonal: the 8 threads of a quarter warp read 8 distinct bank groups
         const uint4 x = row[q];
-        lo += (x.x & 0xFFFFu) + (x.y & 0xFFFFu) + (x.z & 0xFFFFu) + (x.w & 0xFFFFu);
-        hi += (x.x >> 16) + (x.y >> 16) + (x.z >> 16) + (x.w >> 16);
+        // word = P + kF1NegInc * N with P + N <= 65024 < kF1NegInc: N = word / kF1NegInc exactly
+        const uint32_t n0 = x.x / kF1NegInc, n1 = x.y / kF1NegInc, n2 = x.z / kF1NegInc, n3 = x.w / kF1NegInc;
+        hi += n0 + n1 + n2 + n3;
+        lo += (x.x - n0 * kF1NegInc) + (x.y - n1 * kF1NegInc) + (x.z - n2 * kF1NegInc) + (x.w - n3 * kF1NegInc);
         row[q] = make_uint4(0, 0, 0, 0);
       }
       acc[2 * j] += lo;
@@ -316,11 +323,13 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
           // counter half) from one PRMT sign-replicate + 1.  F1 is ALU-pipe bound otherwise.
           const uint32_t rh = __umulhi(rc, k16);
           const uint32_t rl = rc & 0xFFFFu;
-          uint32_t mlo, mhi;
-          asm("prmt.b32 %0, %1, 0, 0x4499;" : "=r"(mlo) : "r"(x));
-          asm("prmt.b32 %0, %1, 0, 0x44BB;" : "=r"(mhi) : "r"(x));
-          red_add_shared(rl * k128 + base, mlo + 1u);
-          red_add_shared(rh * k128 + base, mhi + 1u);
+          // increment 1 (positive pattern) or kF1NegInc = 0xFF01 (negative) in ONE PRMT: byte 0
+          // from the constant 1, byte 1 the sign of the pattern replicated, bytes 2-3 zero
+          uint32_t ilo, ihi;
+          asm("prmt.b32 %0, %1, %2, 0x5594;" : "=r"(ilo) : "r"(x), "r"(1u));
+          asm("prmt.b32 %0, %1, %2, 0x55B4;" : "=r"(ihi) : "r"(x), "r"(1u));
+          red_add_shared(rl * k128 + base, ilo);
+          red_add_shared(rh * k128 + base, ihi);
         }
         if (max(rmax2 & 0xFFFFu, rmax2 >> 16) >= (uint32_t)kF1LRows) {
 #pragma unroll
