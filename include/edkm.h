@@ -120,6 +120,17 @@ typedef struct {
 } edkm_nvls;
 edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* nvls, void* stream);
 
+/* Timeout of edkm_uniquify_nvls's arrival barrier (host-side setting for later calls; default
+ * 20 s with trap = 1: a timed-out wait traps -- the process fails loudly instead of hanging).
+ * trap = 0: a timed-out wait records the failure and the stream continues (the counts are then
+ * wrong) -- for a first call that checks whether the NVLS exchange works at all and falls back
+ * to edkm_uniquify + an all-reduce if not.  EDKM_E_ARG if seconds <= 0 or NaN. */
+edkm_status edkm_nvls_set_timeout(double seconds, int trap);
+
+/* *failed = 1 if a non-trapping NVLS wait timed out since the last call (then clears it).
+ * Synchronous (reads a device flag of the current device).  EDKM_E_ARG if failed is NULL. */
+edkm_status edkm_nvls_failed(int* failed);
+
 /* NVLS multicast buffers backing edkm_nvls (driver-API plumbing; no compute).
  *   edkm_mc_supported : *supported = 1 if the current device supports multicast objects.
  *   edkm_mc_create    : rank 0 -- a multicast object of >= bytes for nranks GPUs (size rounded

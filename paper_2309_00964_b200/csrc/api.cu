@@ -213,6 +213,19 @@ edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_
   return EDKM_OK;
 }
 
+edkm_status edkm_nvls_set_timeout(double seconds, int trap) {
+  if (!(seconds > 0.0)) return fail(EDKM_E_ARG, "NVLS timeout must be > 0");
+  nvls_set_timeout(seconds, trap);
+  return EDKM_OK;
+}
+
+edkm_status edkm_nvls_failed(int* failed) {
+  if (!failed) return fail(EDKM_E_ARG, "NULL failed");
+  cudaError_t e = nvls_failed(failed);
+  if (e != cudaSuccess) return cuda_fail(e, "read NVLS status");
+  return EDKM_OK;
+}
+
 edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* x, void* stream) {
   g_launches = 0;
   if (wdtype != EDKM_BF16 && wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");

@@ -49,6 +49,8 @@ struct B2Args {
   const TensorState* state; // [nt]: the magnitude-page windows
 };
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s);
+void nvls_set_timeout(double seconds, int trap);
+cudaError_t nvls_failed(int* failed);
 cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
                            uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s);
 cudaError_t launch_f2(const StreamArgs& A, const F2Args& F, int mode, int sms, cudaStream_t s);

@@ -248,8 +248,16 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
 // NVLS mode: wait until every CTA of every rank has arrived for this step (counter >= nranks *
 // epoch, monotonic, never reset, so a fast rank's next-step arrivals cannot be lost), then
 // advance this rank's epoch.  One CTA; the acquire loads order the reads of the counts after it.
-__global__ void f1_nvls_wait_kernel(const uint32_t* flags, int nflags, uint32_t* epoch, uint32_t nranks) {
+// On timeout (a rank is gone, or multicast reductions do not arrive): trap -- fail loudly instead
+// of hanging -- or, for a self-check that must be able to fall back (trap = 0), record the
+// failure in g_nvls_failed (edkm_nvls_failed) and let the stream continue.
+__device__ uint32_t g_nvls_failed;
+__global__ void f1_nvls_wait_kernel(const uint32_t* flags, int nflags, uint32_t* epoch, uint32_t nranks,
+                                    uint64_t timeout_ns, int trap) {
   const uint32_t e = *epoch + 1u, target = e * nranks;
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int c = threadIdx.x; c < nflags; c += blockDim.x) {
@@ -259,15 +267,22 @@ __global__ void f1_nvls_wait_kernel(const uint32_t* flags, int nflags, uint32_t*
       if ((int32_t)(v - target) >= 0) break;
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 20000000000ull) {  // 20 s: a rank is gone -- fail loudly instead of hanging
-        printf("edkm: NVLS arrival barrier timed out (counter %d = %u, waiting for %u)\n", c, v, target);
-        asm volatile("trap;");
+      if (now - t0 > timeout_ns || *(volatile int*)&s_fail) {
+        if (trap) {
+          printf("edkm: NVLS arrival barrier timed out (counter %d = %u, waiting for %u)\n", c, v, target);
+          asm volatile("trap;");
+        }
+        s_fail = 1;
+        break;
       }
       __nanosleep(64);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *epoch = e;
+  if (threadIdx.x == 0) {
+    if (s_fail) atomicExch(&g_nvls_failed, 1u);
+    *epoch = e;
+  }
 }
 
 template <int MC>
@@ -871,6 +886,20 @@ cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_
 
 // NVLS mode: grid = `sms` CTAs on every rank (also when this rank's slice is empty), each
 // signalling its arrival counter; then the wait kernel.
+static double g_nvls_timeout_s = 20.0;
+static int g_nvls_trap = 1;
+void nvls_set_timeout(double seconds, int trap) {
+  g_nvls_timeout_s = seconds;
+  g_nvls_trap = trap;
+}
+cudaError_t nvls_failed(int* failed) {
+  uint32_t v = 0, z = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&v, g_nvls_failed, sizeof(v));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_nvls_failed, &z, sizeof(z));
+  *failed = v != 0;
+  return e;
+}
+
 cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
                            uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s) {
   const size_t smem = kF1Smem;
@@ -881,7 +910,8 @@ cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* fl
   else f1_hist_kernel<1><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  f1_nvls_wait_kernel<<<1, 256, 0, s>>>(flags, sms, epoch, (uint32_t)nranks);
+  f1_nvls_wait_kernel<<<1, 256, 0, s>>>(flags, sms, epoch, (uint32_t)nranks, (uint64_t)(g_nvls_timeout_s * 1e9),
+                                        g_nvls_trap);
   return cudaGetLastError();
 }
 

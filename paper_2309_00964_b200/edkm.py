@@ -73,6 +73,8 @@ def lib():
             "edkm_workspace_bytes": ([i32, pp], ctypes.c_size_t),
             "edkm_uniquify": ([P, i32, i32, P, P], i32),
             "edkm_uniquify_nvls": ([P, i32, i32, ctypes.POINTER(_Nvls), P], i32),
+            "edkm_nvls_set_timeout": ([ctypes.c_double, i32], i32),
+            "edkm_nvls_failed": ([P], i32),
             "edkm_forward": ([P, i32, pp, P, P, P, P, P], i32),
             "edkm_forward_range": ([P, i32, i32, i32, pp, P, P, P, P, P], i32),
             "edkm_backward_table_range": ([i32, i32, i32, pp, P, P, P, P, P, P], i32),
@@ -107,7 +109,8 @@ def lib():
 
 
 def exported_symbols() -> list:
-    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_uniquify_nvls", "edkm_forward", "edkm_forward_range",
+    return ["edkm_saved_bytes", "edkm_workspace_bytes", "edkm_uniquify", "edkm_uniquify_nvls", "edkm_nvls_set_timeout",
+            "edkm_nvls_failed", "edkm_forward", "edkm_forward_range",
             "edkm_backward_table_range", "edkm_layout", "edkm_reconstruct",
             "edkm_backward_reduce", "edkm_backward_apply", "edkm_backward", "edkm_backward_buckets",
             "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
@@ -129,6 +132,18 @@ def last_launch_count() -> int:
 def set_max_ctas(ctas: int) -> int:
     """Cap the streaming kernels' grid for later calls on this thread (0 = SM count); returns the old cap."""
     return lib().edkm_set_max_ctas(int(ctas))
+
+
+def nvls_set_timeout(seconds: float, trap: bool = True):
+    """Arrival-barrier timeout of later NVLS uniquify calls (edkm_nvls_set_timeout)."""
+    _check(lib().edkm_nvls_set_timeout(ctypes.c_double(seconds), int(bool(trap))), "edkm_nvls_set_timeout")
+
+
+def nvls_failed() -> bool:
+    """True if a non-trapping NVLS arrival wait timed out since the last call (clears the flag; syncs)."""
+    f = ctypes.c_int(0)
+    _check(lib().edkm_nvls_failed(ctypes.byref(f)), "edkm_nvls_failed")
+    return bool(f.value)
 
 
 @dataclass(frozen=True)

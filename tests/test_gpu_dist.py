@@ -157,7 +157,18 @@ def _nvls_worker(port, q, emulate):
         ref.step(Ws, Gs, C0, outs2, dW2)
         torch.cuda.synchronize()
         same = all(torch.equal(a, b) for a, b in zip(outs + dW, outs2 + dW2)) and torch.equal(plan.dC0, ref.dC0)
-        q.put(("ok", res, bool(same), int(nv.epoch.item())))
+        epoch = int(nv.epoch.item())
+        timeout_ok = None
+        if emulate:
+            # a barrier that can never complete (epoch pushed ahead of every arrival counter) with
+            # trap = 0: the wait gives up after the timeout and reports it instead of trapping
+            E.nvls_set_timeout(0.05, trap=False)
+            nv.epoch += 100
+            plan.uniquify_nvls(Ws, nv)
+            first, second = E.nvls_failed(), E.nvls_failed()
+            E.nvls_set_timeout(20.0, trap=True)
+            timeout_ok = first and not second
+        q.put(("ok", res, bool(same), epoch, timeout_ok))
     finally:
         dist.destroy_process_group()
 
@@ -174,7 +185,9 @@ def test_nvls_fused_counts_world1(emulate):
     pr.join(timeout=120)
     if out[0] == "skip":
         pytest.skip(out[1])
-    _, res, same, epoch = out
+    _, res, same, epoch, timeout_ok = out
     assert all(res), res
     assert same
     assert epoch == 6  # five uniquify_nvls steps + the ShardedStep
+    if emulate:
+        assert timeout_ok  # non-trapping timeout recorded once (edkm_nvls_set_timeout / edkm_nvls_failed)
