@@ -243,6 +243,26 @@ def test_misaligned_slices():
     check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
 
 
+def test_narrow_window_tail_outliers():
+    """Weights whose populated pages span more than the per-weight kernels' window cap (55
+    magnitude pages): TF then picks the narrowest window holding all but ~1e-6 of the weights
+    (common.cuh choose_window), so a handful of tiny-magnitude outliers fall outside it and take
+    the generic paths of B1 (fp64 global bucket), B2 (global (phi, psi)) and F1/F2 -- the
+    results must still match the oracle element by element."""
+    n = 1 << 23
+    W = synth.normal_tensor(n, 1.0, torch.bfloat16, 21).clone()
+    G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 22)
+    for i, v in zip((5, 77_777, 1_000_003, 4_000_001, 6_543_210, n - 1), (1e-30, -2e-35, 3e-25, -1e-37, 5e-33, -7e-28)):
+        W[i] = v
+    wb = bits_of(W)
+    pages = np.unique((wb >> 8) & 0x7F)
+    assert pages.max() - pages.min() + 1 > 55  # the window must be narrowed
+    p = E.Params(torch.bfloat16, 3, 1e-3, 5)
+    C0 = synth.quantile_centroids(8, 1.0)
+    gpu = run_gpu([W], [G], [C0], p)
+    check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
+
+
 # --------------------------------------------------------------------------- histogram edge cases (bit-exact)
 @pytest.mark.parametrize("case", ["constant", "every_pattern", "random_bits", "signed_zero", "tiny", "big"])
 def test_uniquify_edge_cases(case):
