@@ -449,6 +449,21 @@ class Plan:
         self.backward_apply(weights, grads, dW, stream)
         return self.dC0
 
+    def graph(self, weights, grads, C0, outs, dW, allreduce=None):
+        """Capture one `step` over these buffers into a CUDA graph and return it (a
+        torch.cuda.CUDAGraph): `replay()` re-runs the whole step -- memsets, the seven kernels and
+        the collectives, if any -- with no per-launch host work.  Each replay reads whatever the
+        captured input tensors (weights, grads, C0) hold and writes the captured outputs."""
+        side = torch.cuda.Stream(self.counts.device)
+        side.wait_stream(torch.cuda.current_stream(self.counts.device))
+        with torch.cuda.stream(side):  # one eager step first: kernel attributes, cached pointer arrays
+            self.step(weights, grads, C0, outs, dW, allreduce)
+        torch.cuda.current_stream(self.counts.device).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(weights, grads, C0, outs, dW, allreduce)
+        return g
+
 
 # ----------------------------------------------------------------------------- autograd wrapper
 class EDKMFunction(torch.autograd.Function):

@@ -263,6 +263,40 @@ def test_narrow_window_tail_outliers():
     check_tensor(gpu, 0, wb, G.double().numpy(), oracle_dense(wb, G.double().numpy(), C0, p), p)
 
 
+def test_cuda_graph_replay_matches_eager():
+    """Plan.graph: the whole step captured once and replayed on new input values gives the
+    eager step's results (counts, W~ bit-exact; the gradients to fp64 atomic-order rounding)."""
+    dev = torch.device("cuda")
+    sizes = [300_001, 1 << 20, 4097]
+    p = E.Params(torch.bfloat16, 3, 1e-3, 5)
+    C0 = torch.tensor([synth.quantile_centroids(8, 1.0)] * len(sizes), dtype=torch.float32, device=dev)
+
+    def inputs(seed):
+        return ([synth.normal_tensor(n, 1.0, torch.bfloat16, seed + i).to(dev) for i, n in enumerate(sizes)],
+                [synth.normal_tensor(n, 1e-3, torch.bfloat16, seed + 50 + i).to(dev) for i, n in enumerate(sizes)])
+
+    Ws, Gs = inputs(100)
+    outs = [torch.empty(n, dtype=torch.float32, device=dev) for n in sizes]
+    dW = [torch.empty(n, dtype=torch.float32, device=dev) for n in sizes]
+    plan = E.Plan(sizes, p, dev)
+    g = plan.graph(Ws, Gs, C0, outs, dW)
+    W2, G2 = inputs(200)  # new values in the captured buffers
+    for a, b in zip(Ws + Gs, W2 + G2):
+        a.copy_(b)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = E.Plan(sizes, p, dev)
+    outs2 = [torch.empty_like(o) for o in outs]
+    dW2 = [torch.empty_like(d) for d in dW]
+    ref.step(W2, G2, C0, outs2, dW2)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.counts, ref.counts)
+    assert all(torch.equal(a, b) for a, b in zip(outs, outs2))
+    for a, b in zip(dW, dW2):
+        assert normwise(a.cpu().double().numpy(), b.cpu().double().numpy()) <= 1e-12
+    assert normwise(plan.dC0.cpu().double().numpy(), ref.dC0.cpu().double().numpy()) <= 1e-9
+
+
 # --------------------------------------------------------------------------- histogram edge cases (bit-exact)
 @pytest.mark.parametrize("case", ["constant", "every_pattern", "random_bits", "signed_zero", "tiny", "big"])
 def test_uniquify_edge_cases(case):
