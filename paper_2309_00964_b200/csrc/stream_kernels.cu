@@ -152,7 +152,9 @@ constexpr int kF1LRows = kF1LPages * 256;  // 1792 words per copy, 32 copies = 2
 // vectors per thread between folds (32*127*16 < 65536); measured: 4x fewer folds would save
 // only ~3% of F1, not worth an unsafe bound
 constexpr int kF1LChunkVec = 127;
-constexpr int kF1Sample = 16384;
+// patterns sampled per segment to place the window (4 per thread, one round of loads; 16K
+// measured ~3% slower on CFG2's F1 and no better a window)
+constexpr int kF1Sample = 4096;
 // Lane-private counter word = P + kF1NegInc * N (P, N: counts of the positive and negative
 // pattern of the row since the last fold, P + N <= 32 * kF1LChunkVec * 16 = 65024 < kF1NegInc,
 // so the word is < 2^32 and decodes exactly).  The increment 1 or 0xFF01 is one PRMT.
@@ -191,7 +193,7 @@ __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
   }
 }
 
-// F1's window: the kF1LPages consecutive magnitude pages holding most of a 16K-pattern sample of
+// F1's window: the kF1LPages consecutive magnitude pages holding most of a 4K-pattern sample of
 // the segment [a, b), and whether the lane-private path pays (every thread calls it; the result
 // is in *s_base / *s_lp after the closing barrier).
 __device__ __forceinline__ void f1_choose_window(const uint16_t* w, int64_t a, int64_t b, int wdtype, uint32_t* s_pg,
