@@ -216,9 +216,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # under torchrun: always use the process group
     distributed = world > 1 or launched
+    # EDKM_DIST_BACKEND=gloo: a check of the multi-rank orchestration with every rank on the GPUs
+    # there are (e.g. two ranks sharing one B200); the bench itself uses NCCL, one rank per GPU
+    backend = os.environ.get("EDKM_DIST_BACKEND", "nccl")
+    if distributed and backend != "nccl":
+        local = local % torch.cuda.device_count()
     if distributed:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if rank == 0:
         B.build()
     if distributed:
@@ -258,9 +266,26 @@ def main():
     views = plan.views() if shard else None
     stream = torch.cuda.current_stream()
 
-    def allreduce(t):
-        if distributed:
-            dist.all_reduce(t)
+    def allreduce(t, op=None):
+        op = dist.ReduceOp.SUM if op is None else op
+        if not distributed:
+            return
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:  # gloo check mode: through host memory
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+
+    def allgather(full):
+        if backend == "nccl":
+            return allgather_blocks(full)
+        P = dist.get_world_size()  # gloo check mode: rank blocks through host memory
+        b = full.shape[0] // P
+        parts = [torch.empty_like(full[:b], device="cpu") for _ in range(P)]
+        dist.all_gather(parts, full[rank * b:(rank + 1) * b].cpu())
+        full.copy_(torch.cat(parts))
+        return full
 
     # N > 1: exchange 1 fused into F1 over NVLS (dist.NvlsCounts) when the system supports it and
     # it passes a bit-exact self-check against F1 + NCCL all-reduce; otherwise NCCL.
@@ -280,7 +305,7 @@ def main():
             allreduce(want)
             ok = torch.tensor([float(not timed_out and torch.equal(got, want))], device=dev)
             if distributed:
-                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                allreduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() != 1.0:
                 raise RuntimeError("NVLS counts differ from the NCCL all-reduce")
             exchange = "counts: NVLS multimem reductions fused into F1 + in-kernel arrival barrier; gamma: nccl all-reduce"
@@ -307,7 +332,7 @@ def main():
         if shard:
             plan.forward_range(t0, t1, C0)   # TF, this rank's tensor block
             for name in ("state", "ctraj", "rows", "page_cnt", "C_out", "table16"):
-                allgather_blocks(views[name])
+                allgather(views[name])
         else:
             plan.forward(C0)                 # TF
         mark(3)
@@ -322,7 +347,7 @@ def main():
         if shard:
             plan.backward_table_range(t0, t1)  # TB, this rank's tensor block
             for name in ("phipsi", "dC0"):
-                allgather_blocks(views[name])
+                allgather(views[name])
         else:
             plan.backward_table()            # TB
         mark(8)
@@ -352,7 +377,7 @@ def main():
              for i, n in enumerate(names)}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     launches_per_step = 7 + (nv is not None)  # + the NVLS arrival-barrier kernel
 
@@ -406,9 +431,12 @@ def main():
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
         if distributed:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        bytes_in = sum(w.numel() * 2 + g.numel() * 2 for w, g in zip(Ws, Gs))
-        bytes_out = sum(w.numel() * 2 * 2 for w in Ws)
+            allreduce(te, op=dist.ReduceOp.MAX)
+        # whole-job bytes (every rank copies its own slices)
+        nb = torch.tensor([sum(w.numel() * 2 + g.numel() * 2 for w, g in zip(Ws, Gs)),
+                           sum(w.numel() * 2 * 2 for w in Ws)], dtype=torch.float64, device=dev)
+        allreduce(nb)
+        bytes_in, bytes_out = int(nb[0].item()), int(nb[1].item())
         e2e = {"value": n_total / (float(te.item()) / 1e3), "unit": "weights/s", "h2d_bytes_per_step": bytes_in,
                "d2h_bytes_per_step": bytes_out, "ms_per_step": float(te.item()), "steps": args.e2e_steps,
                "path": f"pipeline.HostPipeline ({args.e2e_groups} tensor groups; H2D, the C-ABI step and D2H overlap on 3 streams); pinned host W, G in and W~, dW out every step"}
