@@ -33,10 +33,17 @@ namespace edkm {
 #define EDKM_FTHREADS 256
 #endif
 constexpr int kFThreads = EDKM_FTHREADS;  // TF, TGAMMA: small shared footprint, two CTAs per SM
-constexpr int kBThreads = 512;  // TB: 192 KiB of staged rows, one CTA per SM
-constexpr int kStage = 12288;  // rows per CTA staged in shared memory: value (f32), count (i32), psi (f64)
+// TB comes in two shapes, chosen by the weights' dtype (the host does not know U):
+//   large: 512 threads, 12288 staged rows (192 KiB), one CTA per SM -- fp16 (U ~ 24K per tensor)
+//   small: 256 threads, 4608 staged rows (72 KiB), two CTAs per SM -- bf16 (U ~ 5K): two CTAs of
+//          different tensors interleave their per-iteration barriers (CFG3 TB 0.29 -> 0.245 ms;
+//          for fp16 the rows beyond the stage take the global path and it measured slower)
+// Rows beyond the stage are always correct (read from global memory), so the choice is a
+// performance one only.
+constexpr int kStage = 12288;  // TF: rows per CTA staged in shared memory: value (f32), count (i32)
 constexpr size_t kStageBytesF = (size_t)kStage * 8;   // TF: value + count
-constexpr size_t kStageBytesB = (size_t)kStage * 16;  // TB: value + count + psi
+constexpr int kBThreadsL = 512, kStageBL = 12288;      // TB large: value (f32), count (i32), psi (f64)
+constexpr int kBThreadsS = 256, kStageBS = 4608;       // TB small
 
 // Centroids of one iteration in the forms the attention needs: fp64 values, fp32 values
 // (to pick the nearest centroid), and per centroid pair (m, j) the fp64-derived difference
@@ -163,12 +170,12 @@ struct RowStage {
   int32_t* sn;   // [kStage] count n_u
   double* spsi;  // [kStage] psi accumulator (TB)
   double* gpsi;  // global psi for r >= kStage
-  int nr, wdtype;
-  __device__ __forceinline__ double v(int r) const { return r < kStage ? (double)sv[r] : decode16(rows[r], wdtype); }
-  __device__ __forceinline__ double n(int r) const { return (double)(r < kStage ? sn[r] : cnt[rows[r]]); }
-  __device__ __forceinline__ double& psi(int r) const { return r < kStage ? spsi[r] : gpsi[r]; }
+  int nr, wdtype, ns;  // ns: staged capacity
+  __device__ __forceinline__ double v(int r) const { return r < ns ? (double)sv[r] : decode16(rows[r], wdtype); }
+  __device__ __forceinline__ double n(int r) const { return (double)(r < ns ? sn[r] : cnt[rows[r]]); }
+  __device__ __forceinline__ double& psi(int r) const { return r < ns ? spsi[r] : gpsi[r]; }
   __device__ void stage() {
-    for (int r = threadIdx.x; r < nr && r < kStage; r += blockDim.x) {
+    for (int r = threadIdx.x; r < nr && r < ns; r += blockDim.x) {
       const uint32_t u = rows[r];
       sv[r] = decode16f(u, wdtype);
       sn[r] = cnt[u];
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
     }
   }
   RowStage R{rows, cnt, reinterpret_cast<float*>(stage_mem), reinterpret_cast<int32_t*>(stage_mem) + kStage, nullptr,
-             nullptr, nr, P.wdtype};
+             nullptr, nr, P.wdtype, kStage};
   R.stage();
 
   // ---- 2. unrolled centroid updates
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(kFThreads) tgamma_kernel(const TableArgs P) {
 }
 
 // ============================================================================ TB
-template <int K>
+template <int K, int kBThreads, int kStageB>
 __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
@@ -442,9 +449,9 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   // heuristic in TF) that is the single partition `crank`, staged in shared memory
   const bool one = pcl == cl;
   const int pb0 = one ? st->pbase[crank] : 0;
-  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem + kStage),
-             reinterpret_cast<int32_t*>(stage_mem + kStage) + kStage, stage_mem, psi + pb0,
-             one ? st->nrows[crank] : 0, P.wdtype};
+  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem + kStageB),
+             reinterpret_cast<int32_t*>(stage_mem + kStageB) + kStageB, stage_mem, psi + pb0,
+             one ? st->nrows[crank] : 0, P.wdtype, kStageB};
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
@@ -590,6 +597,21 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
 
 EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytesF, kFThreads)
 EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
-EDKM_TABLE_LAUNCH(launch_tb, tb_kernel, kStageBytesB, kBThreads)
+template <int K>
+static cudaError_t launch_tb_k(const TableArgs& P, cudaStream_t s) {
+  if (P.wdtype == kBF16)
+    return launch_table(P, s, tb_kernel<K, kBThreadsS, kStageBS>, (size_t)kStageBS * 16, kBThreadsS);
+  return launch_table(P, s, tb_kernel<K, kBThreadsL, kStageBL>, (size_t)kStageBL * 16, kBThreadsL);
+}
+
+cudaError_t launch_tb(const TableArgs& P, cudaStream_t s) {
+  switch (P.k) {
+    case 2: return launch_tb_k<2>(P, s);
+    case 4: return launch_tb_k<4>(P, s);
+    case 8: return launch_tb_k<8>(P, s);
+    case 16: return launch_tb_k<16>(P, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 }  // namespace edkm
