@@ -40,8 +40,10 @@ constexpr int kFThreads = EDKM_FTHREADS;  // TF, TGAMMA: small shared footprint,
 //          for fp16 the rows beyond the stage take the global path and it measured slower)
 // Rows beyond the stage are always correct (read from global memory), so the choice is a
 // performance one only.
-constexpr int kStage = 12288;  // TF: rows per CTA staged in shared memory: value (f32), count (i32)
-constexpr size_t kStageBytesF = (size_t)kStage * 8;   // TF: value + count
+// TF: rows per CTA staged in shared memory (value f32, count i32): 12288 (96 KiB, two CTAs per
+// SM) for fp16; 4608 rows (36 KiB) and at most 64 registers, four CTAs per SM, for bf16
+// (CFG3 TF 0.165 -> 0.142 ms; rows beyond the stage take the global path, so never wrong)
+constexpr int kStageFL = 12288, kStageFS = 4608;
 constexpr int kBThreadsL = 512, kStageBL = 12288;      // TB large: value (f32), count (i32), psi (f64)
 constexpr int kBThreadsS = 256, kStageBS = 4608;       // TB small
 
@@ -185,8 +187,8 @@ struct RowStage {
 };
 
 // ============================================================================ TF
-template <int K>
-__global__ void __launch_bounds__(kFThreads) tf_kernel(const TableArgs P) {
+template <int K, int kStage, int kMinBlocks>
+__global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
@@ -595,7 +597,22 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
     }                                                            \
   }
 
-EDKM_TABLE_LAUNCH(launch_tf, tf_kernel, kStageBytesF, kFThreads)
+template <int K>
+static cudaError_t launch_tf_k(const TableArgs& P, cudaStream_t s) {
+  if (P.wdtype == kBF16)
+    return launch_table(P, s, tf_kernel<K, kStageFS, 4>, (size_t)kStageFS * 8, kFThreads);
+  return launch_table(P, s, tf_kernel<K, kStageFL, 2>, (size_t)kStageFL * 8, kFThreads);
+}
+
+cudaError_t launch_tf(const TableArgs& P, cudaStream_t s) {
+  switch (P.k) {
+    case 2: return launch_tf_k<2>(P, s);
+    case 4: return launch_tf_k<4>(P, s);
+    case 8: return launch_tf_k<8>(P, s);
+    case 16: return launch_tf_k<16>(P, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
 template <int K>
 static cudaError_t launch_tb_k(const TableArgs& P, cudaStream_t s) {
