@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
 
 // ============================================================================ TGAMMA
 template <int K>
-__global__ void __launch_bounds__(kFThreads) tgamma_kernel(const TableArgs P) {
+__global__ void __launch_bounds__(kFThreads, K <= 8 ? 4 : 2) tgamma_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   __shared__ double red[(kFThreads / 32) * K], part[2 * K], tot[K];
