@@ -99,7 +99,7 @@ TableArgs table_args(int nt, const edkm_params* p, const void* saved) {
   P.k = 1 << p->bits;
   P.wdtype = p->wdtype;
   P.max_iter = p->max_iter;
-  P.cl = table_cluster_size(nt);
+  P.cl = table_cluster_size(nt, p->wdtype);
   P.tau = p->tau;
   P.inv_tau = 1.0 / p->tau;
   P.eps = p->eps;
@@ -133,7 +133,7 @@ TableArgs table_range(const TableArgs& P, int t0, int t1) {
   const int64_t k = P.k, sc = (int64_t)(P.max_iter + 1) * k, ss = (int64_t)(P.max_iter > 0 ? P.max_iter : 1) * k;
   const int64_t u = (int64_t)t0 * kPatterns;
   R.nt = t1 - t0;
-  R.cl = table_cluster_size(R.nt);
+  R.cl = table_cluster_size(R.nt, P.wdtype);
   R.counts = off(P.counts, u);
   R.C0 = off(P.C0, t0 * k);
   R.C_out = off(P.C_out, t0 * k);

@@ -78,7 +78,7 @@ struct TableArgs {
   double* gamma;           // [nt][k]
   float* dC0;              // [nt][k]
 };
-int table_cluster_size(int nt);
+int table_cluster_size(int nt, int wdtype);
 cudaError_t launch_tf(const TableArgs& P, cudaStream_t s);
 cudaError_t launch_tgamma(const TableArgs& P, cudaStream_t s);
 cudaError_t launch_tb(const TableArgs& P, cudaStream_t s);

@@ -33,19 +33,16 @@ namespace edkm {
 #define EDKM_FTHREADS 256
 #endif
 constexpr int kFThreads = EDKM_FTHREADS;  // TF, TGAMMA: small shared footprint, two CTAs per SM
-// TB comes in two shapes, chosen by the weights' dtype (the host does not know U):
-//   large: 512 threads, 12288 staged rows (192 KiB), one CTA per SM -- fp16 (U ~ 24K per tensor)
-//   small: 256 threads, 4608 staged rows (72 KiB), two CTAs per SM -- bf16 (U ~ 5K): two CTAs of
-//          different tensors interleave their per-iteration barriers (CFG3 TB 0.29 -> 0.245 ms;
-//          for fp16 the rows beyond the stage take the global path and it measured slower)
-// Rows beyond the stage are always correct (read from global memory), so the choice is a
-// performance one only.
+// TB: 256 threads and two CTAs per SM (their per-iteration barriers interleave; CFG3 TB 0.29 ->
+// 0.24 ms against one 512-thread CTA), with the staged rows sized by the weights' dtype (the
+// host does not know U): 4608 rows (72 KiB) for bf16 (U ~ 5K per tensor, cl = 2), 6400 rows
+// (100 KiB) for fp16 (U ~ 24K, cl = 4).  Rows beyond the stage are read from global memory,
+// so the choice is a performance one only.
 // TF: rows per CTA staged in shared memory (value f32, count i32): 12288 (96 KiB, two CTAs per
 // SM) for fp16; 4608 rows (36 KiB) and at most 64 registers, four CTAs per SM, for bf16
 // (CFG3 TF 0.165 -> 0.142 ms; rows beyond the stage take the global path, so never wrong)
 constexpr int kStageFL = 12288, kStageFS = 4608;
-constexpr int kBThreadsL = 512, kStageBL = 12288;      // TB large: value (f32), count (i32), psi (f64)
-constexpr int kBThreadsS = 256, kStageBS = 4608;       // TB small
+constexpr int kBThreads = 256, kStageB16 = 4608, kStageB32 = 6400;  // TB: value (f32), count (i32), psi (f64)
 
 // Centroids of one iteration in the forms the attention needs: fp64 values, fp32 values
 // (to pick the nearest centroid), and per centroid pair (m, j) the fp64-derived difference
@@ -554,14 +551,15 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
 
 // ============================================================================ launchers
 // CTAs per tensor (row partitions, <= the portable cluster size 8): fill the GPU for small nt,
-// else 2.  Rows are balanced across the partitions, but each CTA pays fixed costs per iteration
-// (centroid tables, cluster reduction), and a CTA left alone on an SM in a partial last wave runs
-// faster, so more, smaller partitions measured slower for 226 tensors (cl = 5: TF 0.15 -> 0.26 ms,
-// TB 0.27 -> 0.47 ms on CFG3; CFG4 also slower) -- wave quantisation is not the limit here.
-int table_cluster_size(int nt) {
+// else 2 for bf16 and 4 for fp16.  Rows are balanced across the partitions, but each CTA pays
+// fixed costs per iteration (centroid tables, cluster reduction), so for bf16 (U ~ 5K per
+// tensor) more, smaller partitions measured slower for 226 tensors (cl = 5: TF 0.15 -> 0.26 ms,
+// TB 0.27 -> 0.47 ms on CFG3).  fp16 tensors have ~5x the rows (U ~ 24K): with cl = 4 and TB's
+// two-CTAs-per-SM shape, CFG4 (k = 16) TB 4.06 -> 3.76 ms, k = 4 TB 1.93 -> 1.79 ms.
+int table_cluster_size(int nt, int wdtype) {
   if (nt <= 18) return 8;
   if (nt <= 37) return 4;
-  return 2;
+  return wdtype == kFP16 ? 4 : 2;
 }
 
 template <class Fn>
@@ -617,8 +615,8 @@ EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
 template <int K>
 static cudaError_t launch_tb_k(const TableArgs& P, cudaStream_t s) {
   if (P.wdtype == kBF16)
-    return launch_table(P, s, tb_kernel<K, kBThreadsS, kStageBS>, (size_t)kStageBS * 16, kBThreadsS);
-  return launch_table(P, s, tb_kernel<K, kBThreadsL, kStageBL>, (size_t)kStageBL * 16, kBThreadsL);
+    return launch_table(P, s, tb_kernel<K, kBThreads, kStageB16>, (size_t)kStageB16 * 16, kBThreads);
+  return launch_table(P, s, tb_kernel<K, kBThreads, kStageB32>, (size_t)kStageB32 * 16, kBThreads);
 }
 
 cudaError_t launch_tb(const TableArgs& P, cudaStream_t s) {
