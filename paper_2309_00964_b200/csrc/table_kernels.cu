@@ -38,10 +38,11 @@ constexpr int kFThreads = EDKM_FTHREADS;  // TF, TGAMMA: small shared footprint,
 // host does not know U): 4608 rows (72 KiB) for bf16 (U ~ 5K per tensor, cl = 2), 6400 rows
 // (100 KiB) for fp16 (U ~ 24K, cl = 4).  Rows beyond the stage are read from global memory,
 // so the choice is a performance one only.
-// TF: rows per CTA staged in shared memory (value f32, count i32): 12288 (96 KiB, two CTAs per
-// SM) for fp16; 4608 rows (36 KiB) and at most 64 registers, four CTAs per SM, for bf16
-// (CFG3 TF 0.165 -> 0.142 ms; rows beyond the stage take the global path, so never wrong)
-constexpr int kStageFL = 12288, kStageFS = 4608;
+// TF: rows per CTA staged in shared memory (value f32, count i32): 4608 (36 KiB) for bf16 and
+// 6400 (50 KiB) for fp16, with at most 64 registers (four CTAs per SM) except fp16 k = 16
+// (two).  CFG3 TF 0.165 -> 0.142 ms, CFG4 k=4 1.04 -> 0.82 ms; rows beyond the stage take the
+// global path, so never wrong.
+constexpr int kStageFL = 6400, kStageFS = 4608;
 constexpr int kBThreads = 256, kStageB16 = 4608, kStageB32 = 6400;  // TB: value (f32), count (i32), psi (f64)
 
 // Centroids of one iteration in the forms the attention needs: fp64 values, fp32 values
@@ -599,7 +600,8 @@ template <int K>
 static cudaError_t launch_tf_k(const TableArgs& P, cudaStream_t s) {
   if (P.wdtype == kBF16)
     return launch_table(P, s, tf_kernel<K, kStageFS, 4>, (size_t)kStageFS * 8, kFThreads);
-  return launch_table(P, s, tf_kernel<K, kStageFL, 2>, (size_t)kStageFL * 8, kFThreads);
+  // fp16: ~6K rows per CTA at cl = 4; four CTAs per SM where k <= 8 fits 64 registers
+  return launch_table(P, s, tf_kernel<K, kStageFL, (K <= 8 ? 4 : 2)>, (size_t)kStageFL * 8, kFThreads);
 }
 
 cudaError_t launch_tf(const TableArgs& P, cudaStream_t s) {
