@@ -85,8 +85,12 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--weights", type=float, default=6738149376)
     ap.add_argument("--tag", default="r01")
-    ap.add_argument("--peak", type=float, default=6539.5)
+    ap.add_argument("--peak", type=float, default=None,
+                    help="HBM GB/s (default: hbm_gbs of MEASURED_PEAKS.json, the driver's measurement)")
     a = ap.parse_args()
+    if a.peak is None:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            a.peak = float(json.load(f)["hbm_gbs"])
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lines = [f"# ncu summary {a.tag}", ""]
     js = {"tag": a.tag, "weights": a.weights, "peak_gbs": a.peak, "kernels": {}}
