@@ -56,15 +56,19 @@ struct CSet {
   int sidx[K];   // ... and their indices: nearest-centroid search by bisection
   float dms[K][K];
   float ph[K][K], pl[K][K];
+  float dpl[K][K];  // dms * pl (rounded once from fp64): the logit is one FFMA, fma(-dms, 2v - ph, dpl)
   // every thread of the block calls it; the caller synchronises before and after
   __device__ void prepare(const double* src, double inv_tau) {
     const int t = threadIdx.x;
     if (t < K * K) {
       const double a = src[t / K], b = src[t % K], p = a + b;
-      dms[t / K][t % K] = (float)((a - b) * inv_tau * 1.4426950408889634);
+      const float d = (float)((a - b) * inv_tau * 1.4426950408889634);
+      dms[t / K][t % K] = d;
       const float h = (float)p;
       ph[t / K][t % K] = h;
-      pl[t / K][t % K] = (float)(p - (double)h);
+      const float l = (float)(p - (double)h);
+      pl[t / K][t % K] = l;
+      dpl[t / K][t % K] = (float)((double)d * (double)l);
     }
     if (t < K) {
       const double ct = src[t];
@@ -118,17 +122,36 @@ __device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float
   const int jm = cs.nearest(vf);
   const float* dmr = cs.dms[jm];
   const float* phr = cs.ph[jm];
-  const float* plr = cs.pl[jm];
+  const float* dplr = cs.dpl[jm];
   const float v2 = 2.0f * vf;
   float Z = 0.0f;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    A[j] = ex2(-(dmr[j] * ((v2 - phr[j]) - plr[j])));
+    // -(dms (2v - ph - pl)) = fma(-dms, 2v - ph, dms pl): 2v - ph exact where it is small
+    // (Sterbenz, as before), dms pl a small correction rounded once
+    A[j] = ex2(fmaf(-dmr[j], v2 - phr[j], dplr[j]));
     Z += A[j];
   }
   const float iz = 1.0f / Z;
 #pragma unroll
   for (int j = 0; j < K; ++j) A[j] *= iz;
+}
+
+// The same without the fp32 normalisation: returns 1 / sum_j A[j] (TF applies it in fp64).
+template <int K>
+__device__ __forceinline__ float attention_row_raw(float vf, const CSet<K>& cs, float (&A)[K]) {
+  const int jm = cs.nearest(vf);
+  const float* dmr = cs.dms[jm];
+  const float* phr = cs.ph[jm];
+  const float* dplr = cs.dpl[jm];
+  const float v2 = 2.0f * vf;
+  float Z = 0.0f;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    A[j] = ex2(fmaf(-dmr[j], v2 - phr[j], dplr[j]));
+    Z += A[j];
+  }
+  return 1.0f / Z;
 }
 
 // Sum N doubles over the CTA then over the cluster; result in tot[0..N) of every CTA.
@@ -325,13 +348,14 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
 #pragma unroll
     for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
     for (int r = tid; r < nr; r += kFThreads) {
-      const double v = R.v(r), n = R.n(r), nv = n * v;
+      const double v = R.v(r);
       float A[K];
-      attention_row<K>((float)v, cs, A);
+      // 1/Z applied to the count in fp64 (n/Z, n v/Z) instead of to each A_j in fp32
+      const double nz = R.n(r) * (double)attention_row_raw<K>((float)v, cs, A), nvz = nz * v;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        acc[j] = fma((double)A[j], n, acc[j]);
-        acc[K + j] = fma((double)A[j], nv, acc[K + j]);
+        acc[j] = fma((double)A[j], nz, acc[j]);
+        acc[K + j] = fma((double)A[j], nvz, acc[K + j]);
       }
     }
     cluster_allreduce<2 * K, kFThreads / 32>(acc, red, part, tot, it & 1, cluster);
