@@ -536,14 +536,29 @@ __global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_con
 }
 
 // ============================================================================ B1
-// B[u] = sum G_i over this CTA's weights with pattern u, accumulated exactly in
-// 64-bit fixed point (lo: u32, hi: i32) with native shared-memory integer
-// atomics -- sm_100 has no native shared fp32 atomic add (it is a CAS loop).
-// The per-segment scale 2^s maps the largest |G| of a 4K-element sample to
-// [2^21, 2^22); a pattern outside the shared window, an element whose |q|
-// would exceed 2^24, or a non-finite G goes to the fp64 global bucket instead
-// (predicated, correct, slower).  At the end of the segment the exact per-CTA
-// sums are converted to fp64 once and added to the global buckets.
+// B[u] = sum G_i over this CTA's weights with pattern u, accumulated in 32-bit fixed point with
+// native shared-memory integer atomics -- sm_100 has no native shared fp32 (or 64-bit integer)
+// atomic add: ptxas emits a CAS loop for both.
+//
+// Two fixed-point banks per pattern slot (S4 "B1"): the per-segment scale 2^s maps the
+// largest |G| of a 4K-element sample M to [2^21, 2^22).  An element with |G| >= 2^(24-s-f) goes
+// to the coarse bank as q = rint(G 2^s); a smaller one to the fine bank as q = rint(G 2^(s+f)).
+// Every |q| < 2^24.  For 16-bit G this is EXACT (no rounding at all) for every |G| in
+// [2^(7-s-f), 2^(24-s)) ~ [M 2^-(14+f), 4..8 M): a bf16 (fp16) value with |G| >= 2^e has its
+// last significand bit at 2^(e-7) (2^(e-10)), a multiple of 2^-s once e >= 7-s (10-s), which
+// f <= 17 (14) guarantees for every coarse element.  For fp32 G each element is split into both
+// banks: q_c = rint(G 2^s), and the exact residual G 2^s - q_c (|.| <= 1/2) as q_f = rint(. 2^f)
+// with f = 24, so its rounding is below M 2^-46.  A scale set by the sample max alone (one bank,
+// round 1) rounded every element to M 2^-22 in absolute terms: heavy-tailed G (Cauchy,
+// Student-t, log-normal) then put dC_0 over the 1e-5 bar.
+//
+// lo[] starts at 2^31 (slot value = lo - 2^31 plus the carries): a zero-mean running sum then
+// wraps lo only when it leaves (-2^31, 2^31).  The rare carry/borrow out of lo is added to the
+// fp64 global bucket directly as +-2^32 of the bank's unit (exact: a power of two), so no
+// high word is kept in shared memory.  A pattern outside the shared window, an element whose
+// coarse |q| would reach 2^24 (|G| >= 4..8 M), or a non-finite G goes to the fp64 global bucket
+// instead (predicated, correct, slower).  At the end of the segment the per-CTA bank values are
+// converted to fp64 once and added to the global buckets.
 // GDT: gradient dtype (kBF16, kFP16, kFP32).
 #ifndef EDKM_B1_LOOP
 #define EDKM_B1_LOOP 0
@@ -558,23 +573,25 @@ template <int GDT>
 struct B1Policy {
   static constexpr int kLoop = EDKM_B1_LOOP;
   static constexpr int GF32 = GDT == kFP32;
-  static constexpr uint32_t kHiOff = 2 * kB1Pages * 256 * 4;  // byte offset of hi[] from lo[]
-  // lo[] starts at 2^31 (the slot value is hi*2^32 + lo - 2^31): a zero-mean running sum then
-  // wraps lo only when it leaves (-2^31, 2^31), not at every sign change, so the carry/borrow
-  // atomic is rare instead of a second atomic for most warps.
+  // fine-bank shift f (see above): bf16 <= 17, fp16 <= 14 keep every coarse element exact
+  static constexpr int kFine = GDT == kBF16 ? 16 : (GDT == kFP16 ? 14 : 24);
+  static constexpr uint32_t kSlots = 2 * kB1Pages * 256;  // slots per bank
+  static constexpr uint32_t kFOff = kSlots * 4;           // byte offset of the fine bank
   static constexpr uint32_t kLoBias = 0x80000000u;
   static constexpr int kB1Batch = EDKM_B1_BATCH;  // lo atomics in flight per thread
   const StreamArgs& A;
   const B1Args& Bq;
-  uint32_t* lo;
-  int32_t* hi;
+  uint32_t* lo;    // [2][kSlots]: coarse bank, fine bank
   int pbase, np;
-  bool active;   // scale established (some finite nonzero G, representable scale)
-  float scale;   // 2^s
-  uint32_t glim;   // fp32 bits of 2^24 / 2^s: |G| below it has |q| <= 2^24 (fast path)
+  bool active;     // scale established (some finite nonzero G, representable scale)
+  float scale;     // 2^s  (coarse)
+  float scaleF;    // 2^(s+fe)  (fine)
+  float thrF;      // 16-bit G: |G| < thrF -> fine bank (2^(24-s-fe)); fp32 G: 2^fe
+  uint32_t glim;   // fp32 bits of 2^24 / 2^s: |G| below it has coarse |q| < 2^24 (fast path)
   uint32_t glim16; // the same bound for 16-bit G bit patterns (NaN/Inf excluded)
+  uint32_t thrm1;  // 16-bit G: (smallest magnitude pattern >= thrF) - 1, or 0 if that is pattern 0
   uint32_t negpb2; // -pbase*256 in both 16-bit halves
-  double inv_scale;
+  double unitC, unitF;  // 2^-s, 2^-(s+fe): the value of one unit of each bank
   Win win;
   struct Vec { V8 w; V8 g[GF32 ? 2 : 1]; };
   __device__ double* bucket(int t) const { return Bq.B + (int64_t)(A.t0 + t) * kPatterns; }
@@ -588,9 +605,10 @@ struct B1Policy {
     pbase = Bq.state[A.t0 + t].win[0];  // chosen once per tensor by TF (table_windows)
     np = Bq.state[A.t0 + t].win[1];
     uint4* z = reinterpret_cast<uint4*>(lo);
-    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) z[s] = make_uint4(kLoBias, kLoBias, kLoBias, kLoBias);
-    uint4* zh = reinterpret_cast<uint4*>(hi);
-    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) zh[s] = make_uint4(0, 0, 0, 0);
+    for (int s = threadIdx.x; s < 2 * np * 256 / 4; s += blockDim.x) {
+      z[s] = make_uint4(kLoBias, kLoBias, kLoBias, kLoBias);
+      z[s + kSlots / 4] = make_uint4(kLoBias, kLoBias, kLoBias, kLoBias);
+    }
     __syncthreads();  // s_max = 0 before any atomicMax
     // scale from the max finite |G| of a sample (whole segment if the sample is all zero)
     unsigned m = 0;
@@ -609,22 +627,33 @@ struct B1Policy {
     }
     const unsigned mx = s_max;
     active = false;
-    scale = 0.0f;
-    inv_scale = 0.0;
+    scale = scaleF = thrF = 0.0f;
+    unitC = unitF = 0.0;
     glim = 0;
     glim16 = 0;
+    thrm1 = 0;
     if (mx != 0) {
       int e;
       frexpf(__uint_as_float(mx), &e);  // mx in [2^(e-1), 2^e)
       const int s = 22 - e;              // mx * 2^s in [2^21, 2^22)
       if (s <= 126 && s >= -126) {
         active = true;
+        // fine shift, capped so that 2^(s+fe) stays a normal fp32 (tiny gradients, s near 126)
+        const int fe = min(kFine, 127 - s);
         scale = __int_as_float((127 + s) << 23);
-        inv_scale = __longlong_as_double((long long)(1023 - s) << 52);
-        glim = __float_as_uint(16777216.0f * (float)inv_scale);  // exact: power-of-two scaling
+        scaleF = __int_as_float((127 + s + fe) << 23);
+        thrF = GF32 ? __int_as_float((127 + fe) << 23) : __int_as_float((127 + 24 - s - fe) << 23);
+        unitC = __longlong_as_double((long long)(1023 - s) << 52);
+        unitF = __longlong_as_double((long long)(1023 - s - fe) << 52);
+        glim = __float_as_uint(16777216.0f * (float)unitC);  // exact: power-of-two scaling
         const float lim = __uint_as_float(glim);
         if (GDT == kBF16) glim16 = min((glim + 0xFFFFu) >> 16, 0x7F80u);
         else glim16 = lim >= 65504.0f ? 0x7C00u : (uint32_t)__half_as_ushort(__float2half_ru(lim));
+        // thrF is a power of two: its exact bf16 pattern, or the fp16 pattern rounded up (0x0001 when
+        // thrF is below the smallest fp16 subnormal, 0x7C00 = inf when above the largest finite)
+        const uint32_t t16 = GDT == kBF16 ? (__float_as_uint(thrF) >> 16)
+                                          : (uint32_t)__half_as_ushort(__float2half_ru(thrF));
+        thrm1 = t16 ? t16 - 1u : 0u;
       }
     }
     win.init<4>(smem_addr(lo), pbase, np);
@@ -644,16 +673,32 @@ struct B1Policy {
       r.g[0] = ldg_stream8(reinterpret_cast<const uint16_t*>(A.g[t]) + i);
     }
   }
-  // generic element (scalar head/tail, segments without a scale)
+  // the carry (+1) or borrow (-1) out of lo of an add of q that returned `old`: moved to the
+  // global fp64 bucket as +-2^32 units of the bank (exact)
+  __device__ __forceinline__ void carry(double* gB, uint32_t u, int q, uint32_t old, double unit) const {
+    const bool c = old + (uint32_t)q < old;
+    if (c != (q < 0)) atomicAdd(gB + u, c ? 4294967296.0 * unit : -4294967296.0 * unit);
+  }
+  // the bank (fine?) and integer q of a 16-bit-dtype element (|G| < 2^(24-s) assumed)
+  __device__ __forceinline__ int q16(float g, bool& fine) const {
+    fine = fabsf(g) < thrF;
+    return __float2int_rn(g * (fine ? scaleF : scale));
+  }
+  // generic element (scalar head/tail, out-of-window vectors, segments without a scale)
   __device__ __forceinline__ void add_slow(int t, uint32_t u, float g) {
-    const float x = g * scale;
     const int slot = window_slot(u, pbase, np);
-    if (active && slot >= 0 && fabsf(x) < 2147483520.0f) {
-      const int q = __float2int_rn(x);
-      const uint32_t add = (uint32_t)q;
-      const uint32_t old = atomicAdd(&lo[slot], add);
-      const int delta = (int)(old + add < old) - (int)(q < 0);
-      if (delta) atomicAdd(&hi[slot], delta);
+    if (active && slot >= 0 && __float_as_uint(fabsf(g)) < glim) {
+      const uint32_t a = smem_addr(lo) + (uint32_t)slot * 4u;
+      if (GF32) {
+        const float x = g * scale, xr = rintf(x);
+        const int qc = (int)xr, qf = __float2int_rn((x - xr) * thrF);
+        carry(bucket(t), u, qc, atom_add_shared(a, (uint32_t)qc), unitC);
+        carry(bucket(t), u, qf, atom_add_shared(a + kFOff, (uint32_t)qf), unitF);
+      } else {
+        bool fine;
+        const int q = q16(g, fine);
+        carry(bucket(t), u, q, atom_add_shared(a + (fine ? kFOff : 0u), (uint32_t)q), fine ? unitF : unitC);
+      }
     } else if (g != 0.0f) {
       atomicAdd(&bucket(t)[u], (double)g);
     }
@@ -663,12 +708,70 @@ struct B1Policy {
     if (GDT == kBF16) return __uint_as_float((e & 1) ? (r.g[0].x[e >> 1] & 0xFFFF0000u) : (r.g[0].x[e >> 1] << 16));
     return decode16f(pat(r.g[0], e), kFP16);
   }
+  // The lo atomics of one vector, kB1Batch in flight per thread before any return value is looked
+  // at, then the (rare) carries.  MODE 0: every element to the coarse bank (16-bit G, no nonzero
+  // |G| below thrF: the common case, one FMUL + F2I + atomic per element); 1: per-element bank
+  // choice (16-bit G with some small nonzero |G|); 2: both banks, split (fp32 G).
+  template <int MODE>
+  __device__ __forceinline__ void accumulate(int t, const Vec& r, const uint32_t (&slot2)[8]) {
+    constexpr int kPer = MODE == 2 ? 2 : 1;  // atomics per element
+    constexpr int kEl = kB1Batch / kPer;     // elements per batch
+#pragma unroll
+    for (int h = 0; h < 16; h += kEl) {
+      uint32_t old[kB1Batch];
+      int qv[kB1Batch];
+#pragma unroll
+      for (int e = h; e < h + kEl; ++e) {
+        const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
+        const uint32_t a = win.baseP + slot * 4;
+        const float g = g_of(r, e);
+        if (MODE == 2) {
+          const float x = g * scale, xr = rintf(x);
+          qv[2 * (e - h)] = (int)xr;
+          qv[2 * (e - h) + 1] = __float2int_rn((x - xr) * thrF);
+          old[2 * (e - h)] = fixed_lo(a, qv[2 * (e - h)]);
+          old[2 * (e - h) + 1] = fixed_lo(a + kFOff, qv[2 * (e - h) + 1]);
+        } else if (MODE == 1) {
+          bool fine;
+          qv[e - h] = q16(g, fine);
+          old[e - h] = fixed_lo(a + (fine ? kFOff : 0u), qv[e - h]);
+        } else {
+          qv[e - h] = __float2int_rn(g * scale);
+          old[e - h] = fixed_lo(a, qv[e - h]);
+        }
+      }
+      // |q| < 2^24 here, so lo can only have wrapped if the old value lay within 2^25 of the
+      // 2^32 boundary; lo starts at 2^31 and a zero-mean sum of steps ~2^19 stays far from it,
+      // so the exact carry pass below runs for almost no batch (one min per pair instead of
+      // a carry test per element: B1 was issue-bound on the carry tests).
+      uint32_t near = 0xFFFFFFFFu;
+#pragma unroll
+      for (int e = 0; e < kB1Batch; e += 2) near = min(near, min(old[e] + 0x02000000u, old[e + 1] + 0x02000000u));
+      if (near < 0x04000000u) {
+        double* gB = bucket(t);
+#pragma unroll
+        for (int e = h; e < h + kEl; ++e) {
+          const uint32_t u = pat(r.w, e);
+          if (MODE == 2) {
+            carry(gB, u, qv[2 * (e - h)], old[2 * (e - h)], unitC);
+            carry(gB, u, qv[2 * (e - h) + 1], old[2 * (e - h) + 1], unitF);
+          } else if (MODE == 1) {
+            carry(gB, u, qv[e - h], old[e - h], fabsf(g_of(r, e)) < thrF ? unitF : unitC);
+          } else {
+            carry(gB, u, qv[e - h], old[e - h], unitC);
+          }
+        }
+      }
+    }
+  }
   __device__ void process(int t, int64_t i, const Vec& r) {
     // Window offsets of the 16 patterns two at a time (16x2 SIMD): rel = (u & 0x7FFF) - pbase*256
     // and slot = sign * np*256 + rel; one range check per vector (every rel < np*256 and every
-    // |G| below the overflow limit, NaN/Inf included) selects the fast path.
+    // |G| below the overflow limit, NaN/Inf included) selects the fast path.  For 16-bit G the
+    // same pass takes the minimum of |G| - 1 per half (zero wraps to 0xFFFF: a zero G adds nothing
+    // to either bank), so one compare tells whether every nonzero |G| is >= thrF (coarse bank only).
     uint32_t slot2[8];
-    uint32_t rmax2 = 0, gmax = 0;
+    uint32_t rmax2 = 0, gmax = 0, gmin2 = 0xFFFFFFFFu;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint32_t x = r.w.x[q];
@@ -678,38 +781,16 @@ struct B1Policy {
       if (GF32) {
         gmax = max(gmax, max(r.g[q >> 2].x[(2 * q) & 7] & 0x7FFFFFFFu, r.g[q >> 2].x[(2 * q + 1) & 7] & 0x7FFFFFFFu));
       } else {
-        gmax = __vmaxu2(gmax, r.g[0].x[q] & 0x7FFF7FFFu);
+        const uint32_t m2 = r.g[0].x[q] & 0x7FFF7FFFu;
+        gmax = __vmaxu2(gmax, m2);
+        gmin2 = __vminu2(gmin2, __vsub2(m2, 0x00010001u));
       }
     }
     const bool ok = GF32 ? gmax < glim : (max(gmax & 0xFFFFu, gmax >> 16) < glim16);
     if (active && max(rmax2 & 0xFFFFu, rmax2 >> 16) < win.np256 && ok) {
-      // all 16 lo atomics in flight first, then the (rare) carries: the return latency of
-      // one atomic is not paid per element
-#pragma unroll
-      for (int h = 0; h < 16; h += kB1Batch) {
-        uint32_t old[kB1Batch];
-        int qv[kB1Batch];
-#pragma unroll
-        for (int e = h; e < h + kB1Batch; ++e) {
-          const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
-          qv[e - h] = __float2int_rn(g_of(r, e) * scale);
-          old[e - h] = fixed_lo(win.baseP + slot * 4, qv[e - h]);
-        }
-        // |q| <= 2^24 here, so lo can only have wrapped if the old value lay within 2^25 of the
-        // 2^32 boundary; lo starts at 2^31 and a zero-mean sum of steps ~2^19 stays far from it,
-        // so the exact carry pass below runs for almost no batch (one min per pair instead of
-        // a carry test per element: B1 was issue-bound on the carry tests).
-        uint32_t near = 0xFFFFFFFFu;
-#pragma unroll
-        for (int e = 0; e < kB1Batch; e += 2) near = min(near, min(old[e] + 0x02000000u, old[e + 1] + 0x02000000u));
-        if (near < 0x04000000u) {
-#pragma unroll
-          for (int e = h; e < h + kB1Batch; ++e) {
-            const uint32_t slot = (e & 1) ? (slot2[e >> 1] >> 16) : (slot2[e >> 1] & 0xFFFFu);
-            fixed_carry<kHiOff>(win.baseP + slot * 4, qv[e - h], old[e - h]);
-          }
-        }
-      }
+      if (GF32) accumulate<2>(t, r, slot2);
+      else if (min(gmin2 & 0xFFFFu, gmin2 >> 16) >= thrm1) accumulate<0>(t, r, slot2);
+      else accumulate<1>(t, r, slot2);
     } else {
       // rare: re-read the 16 elements (dynamic indexing of the register vector would spill it)
 #pragma unroll 1
@@ -722,8 +803,8 @@ struct B1Policy {
     if (active) {
       double* Bt = bucket(t);
       for (int s = threadIdx.x; s < 2 * np * 256; s += blockDim.x) {
-        const int64_t v = ((int64_t)hi[s] << 32) + (int64_t)lo[s] - (int64_t)kLoBias;
-        if (v != 0) atomicAdd(&Bt[slot_pattern(s, pbase, np)], (double)v * inv_scale);
+        const int32_t vc = (int32_t)(lo[s] - kLoBias), vf = (int32_t)(lo[s + kSlots] - kLoBias);
+        if (vc != 0 || vf != 0) atomicAdd(&Bt[slot_pattern(s, pbase, np)], (double)vc * unitC + (double)vf * unitF);
       }
     }
     __syncthreads();
@@ -733,7 +814,7 @@ struct B1Policy {
 template <int GDT>
 __global__ void __launch_bounds__(kThreads, 1) b1_bucket_kernel(const __grid_constant__ StreamArgs A, const B1Args Bq) {
   extern __shared__ __align__(16) uint32_t smem_b1[];
-  B1Policy<GDT> p{A, Bq, smem_b1, reinterpret_cast<int32_t*>(smem_b1 + 2 * kB1Pages * 256)};
+  B1Policy<GDT> p{A, Bq, smem_b1};
   for_each_segment(A, p);
 }
 

@@ -86,6 +86,18 @@ def quantile_centroids(k: int, sigma: float) -> list:
     return [nd.inv_cdf((j + 0.5) / k) for j in range(k)]
 
 
+def data_quantile_centroids(w: torch.Tensor, k: int) -> list:
+    """C_0 from the data (R5's alternative for small tensors): the k quantiles of the DISTINCT
+    finite values of w, C_0[j] = d[floor((j + 0.5) m / k)] with d the m sorted distinct values.
+    With m >= k the k centroids are distinct weights, so no cluster starts empty (R6)."""
+    x = w.detach().reshape(-1).double().cpu()
+    d = torch.unique(x[torch.isfinite(x)])
+    m = d.numel()
+    if m == 0:
+        return [0.0] * k
+    return [float(d[min(m - 1, ((2 * j + 1) * m) // (2 * k))]) for j in range(k)]
+
+
 def _gen(device, seed):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -111,6 +123,32 @@ def grads(wl: Workload, t: int, device="cpu", n: int | None = None, dtype=None) 
                          wl.seed_base + 1000 + t, device)
 
 
+HEAVY_TAILS = ("cauchy", "student_t1.2", "lognormal3", "spike")
+
+
+def heavy_tailed(n: int, kind: str, scale: float, dtype: torch.dtype, seed: int) -> torch.Tensor:
+    """n heavy-tailed draws x scale rounded (RNE) to dtype, from a seeded numpy generator (CPU).
+
+    LLM gradients are heavy-tailed; these exercise B1's fixed-point buckets far from the
+    Gaussian law of `grads` (Cauchy, Student-t(1.2), random-sign log-normal(3), and
+    a N(0, 1) tensor with one 1e4x spike inside the first 4,096 elements)."""
+    import numpy as np
+    r = np.random.default_rng(seed)
+    if kind == "cauchy":
+        x = r.standard_cauchy(n)
+    elif kind == "student_t1.2":
+        x = r.standard_t(1.2, n)
+    elif kind == "lognormal3":
+        x = r.lognormal(0.0, 3.0, n) * np.where(r.random(n) < 0.5, -1.0, 1.0)
+    elif kind == "spike":
+        x = r.standard_normal(n)
+        if n:
+            x[min(n - 1, 100)] = 1e4
+    else:
+        raise KeyError(kind)
+    return torch.from_numpy(x * scale).to(dtype)
+
+
 def random_bits(n: int, seed: int, device="cpu") -> torch.Tensor:
     """Uniformly random 16-bit patterns as int16 (every pattern, NaN/Inf included)."""
     return torch.randint(-32768, 32768, (n,), generator=_gen(device, seed), device=device, dtype=torch.int32).to(
@@ -122,4 +160,5 @@ def gib(nbytes: float) -> float:
 
 
 __all__ = ["Workload", "workload", "quantile_centroids", "normal_tensor", "weights", "grads", "random_bits",
+           "heavy_tailed", "HEAVY_TAILS", "data_quantile_centroids",
            "llama_shapes", "LLAMA7B_LAYER", "LLAMA13B_LAYER"]

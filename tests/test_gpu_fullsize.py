@@ -6,8 +6,8 @@ CFG3 (full LLaMA-7B: 226 tensors, 6,738,149,376 bf16 weights, k=8, tau=1e-5, T=5
 Checked against the oracle on sampled tensors, in the attention-table form that
 tests/test_oracle.py pins to the dense definition: exact counts (bit-exact), C_T,
 the W~ table of every populated pattern, dC_0, and 200,000 sampled elements of W~ and dW
-computed one by one from the oracle's (phi, psi).  Every tensor: sum of counts == n and
-no non-finite weights.
+computed one by one from the oracle's (phi, psi).  Every tensor: counts bit-exact against
+the oracle's histogram and no non-finite weights.
 """
 import numpy as np
 import pytest
@@ -42,14 +42,19 @@ def run(name, sample):
     torch.cuda.synchronize()
     nonfin, iters = E.read_status(plan.saved, plan.nt, p)
     counts = plan.counts.cpu().numpy()
-    assert all(int(counts[t].sum()) == Ws[t].numel() for t in range(len(Ws)))
     assert set(iters) == {wl.max_iter} and not any(nonfin)
+    # counts of EVERY tensor bit-exact against the oracle's histogram (F1 is integer work)
+    hist = {}
+    for t in range(len(Ws)):
+        c = O.histogram(Ws[t].view(torch.int16).cpu().numpy().view(np.uint16))
+        assert np.array_equal(counts[t], c.astype(np.int32)), wl.shapes[t][0]
+        if t in sample:
+            hist[t] = c
     rng = np.random.default_rng(7)
     for t in sample:
         bits = Ws[t].view(torch.int16).cpu().numpy().view(np.uint16)
         G = Gs[t].double().cpu().numpy()
-        c = O.histogram(bits)
-        assert np.array_equal(counts[t], c.astype(np.int32)), wl.shapes[t][0]
+        c = hist[t]
         u = np.nonzero(c)[0]
         v = O.decode16(u.astype(np.uint16), O.BF16 if wl.wdtype == torch.bfloat16 else O.FP16)
         C0t = np.float32(C0[t].cpu().numpy()).astype(np.float64)

@@ -371,6 +371,55 @@ def test_eps_stop_self_consistent():
     assert deltas[T - 1] <= eps and np.all(deltas[: T - 1] > eps)
 
 
+def _lloyd_exact(w, C0, T):
+    """Textbook Lloyd k-means in exact rational arithmetic (fractions), independent of the oracle."""
+    from fractions import Fraction
+    C = [Fraction(c) for c in C0]
+    traj = [list(C)]
+    for _ in range(T):
+        a = []
+        for x in w:
+            d = [abs(Fraction(x) - c) for c in C]
+            assert d.count(min(d)) == 1  # no ties: the assignment is unique
+            a.append(d.index(min(d)))
+        C = [sum(Fraction(x) for x, aj in zip(w, a) if aj == j) / max(1, a.count(j)) if j in a else C[j]
+             for j in range(len(C))]
+        traj.append(list(C))
+    return traj
+
+
+@pytest.mark.parametrize("max_iter", [10, 4])
+def test_eps_stop_pinned_to_lloyd(max_iter):
+    """R4 against an independent reference: at tau = 1e-9 the oracle IS Lloyd's k-means (pinned above),
+    so an eps-stopped run must stop after the first update t whose max_j |C_t - C_{t-1}| <= eps, with the
+    deltas taken from textbook Lloyd in exact arithmetic -- not from the oracle's own trajectory.  The
+    data (integers, two clusters whose sizes make every mean dyadic) give exact fp64 deltas 69/8, 7, 5/2,
+    3/2, 5/4, 0, so eps equal to a delta separates `<=` from `<`, and eps just below it from off-by-one."""
+    w = np.array([25, 9, 22, 16, 25, 14, 21, 17], np.float64)
+    C0 = np.array([2.0, 10.0])
+    traj = _lloyd_exact(w.tolist(), C0.tolist(), 10)
+    deltas = [max(abs(a - b) for a, b in zip(traj[t + 1], traj[t])) for t in range(10)]
+    assert [str(d) for d in deltas[:6]] == ["69/8", "7", "5/2", "3/2", "5/4", "0"]
+
+    def expected_T(eps):
+        for t, d in enumerate(deltas[:max_iter]):
+            if d <= eps:
+                return t + 1
+        return max_iter
+
+    cases = [float(d) for d in deltas[:5]]                              # eps exactly a delta
+    cases += [float(np.nextafter(float(d), 0.0)) for d in deltas[:5]]   # just below it
+    cases += [1e-300, 100.0]
+    from fractions import Fraction
+    for eps in cases:
+        Ct, St, T = O.dkm_forward(w, C0, 1e-9, max_iter, eps=eps)
+        assert T == expected_T(Fraction(eps)), (eps, T)
+        np.testing.assert_array_equal(Ct, np.array([[float(c) for c in C] for C in traj[: T + 1]]))
+    # eps = 0 disables the test: exactly max_iter updates
+    _, _, T = O.dkm_forward(w, C0, 1e-9, max_iter, eps=0.0)
+    assert T == max_iter
+
+
 def test_bad_arguments_are_rejected():
     with pytest.raises(ValueError):
         O.dkm_forward([0.0], [0.0], -1.0, 1)
