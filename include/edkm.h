@@ -13,13 +13,14 @@
  *   own bit pattern ("the 16bit value ... can serve as an offset"), so the
  *   index list is W's bytes reinterpreted as uint16 -- no copy is made.
  *   Sharding over learners = each rank passes its contiguous slice of each
- *   tensor; the caller sums `counts` (after edkm_uniquify) and `gamma`
- *   (after edkm_backward_reduce) over ranks, see edkm_backward().
+ *   tensor; `counts` (after F1) and `gamma` (after B1) are summed over ranks --
+ *   by edkm_uniquify / edkm_backward_reduce themselves when given an edkm_comm
+ *   (the NCCL communicator this library owns), or by the caller when comm is NULL.
  *
  * Conventions for every entry point:
  *   - Device pointers unless stated.  The caller owns every buffer; the library
  *     allocates no device memory (except the edkm_mc_* NVLS buffers, on request) and
- *     keeps no state between calls.
+ *     keeps no state between calls other than an edkm_comm (NCCL's own buffers).
  *   - Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
  *     default stream).  No call synchronises the host except edkm_read_status.
  *   - Argument errors (null pointers with n > 0, bad dtype, bits outside 1..8,
@@ -46,10 +47,18 @@ typedef enum {
     EDKM_E_ARG = 1,          /* invalid argument (nothing launched)            */
     EDKM_E_DTYPE = 2,        /* unsupported dtype for this argument            */
     EDKM_E_CUDA = 3,         /* a CUDA launch or API call failed               */
-    EDKM_E_UNSUPPORTED = 4   /* valid request this build does not implement  */
+    EDKM_E_UNSUPPORTED = 4,  /* valid request this build does not implement  */
+    EDKM_E_NCCL = 5          /* an NCCL call failed, or NCCL could not be loaded */
 } edkm_status;
 
-typedef enum { EDKM_BF16 = 0, EDKM_FP16 = 1, EDKM_FP32 = 2, EDKM_U8 = 3 } edkm_dtype;
+typedef enum { EDKM_BF16 = 0, EDKM_FP16 = 1, EDKM_FP32 = 2, EDKM_U8 = 3, EDKM_I32 = 4, EDKM_FP64 = 5 } edkm_dtype;
+typedef enum { EDKM_SUM = 0, EDKM_MAX = 1 } edkm_reduce_op;
+
+/* The NCCL communicator of the learners (P:79 S2.2: "sharded over |L| learners"), owned by the
+ * library -- its only persistent object.  NULL wherever an edkm_comm* is taken = one GPU, no
+ * collective.  With a comm, every rank must make the same calls in the same order with the same
+ * nt and params (collectives), each on its own GPU. */
+typedef struct edkm_comm edkm_comm;
 
 typedef enum {
     EDKM_SOFT = 0,        /* W~_i = table[bits(w_i)] (Fig. 1)                        */
@@ -84,9 +93,11 @@ size_t edkm_workspace_bytes(int nt, const edkm_params* p);
 
 /* F1 -- uniquify.  counts[t*65536 + u] = #{i : bits(w_i) = u} over
  * this rank's slice of tensor t.  counts (int32, [nt][65536]) is overwritten.
- * Exact (integer).  With several ranks the caller sums counts over ranks
- * (integer all-reduce) before edkm_forward. */
-edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, void* stream);
+ * Exact (integer).  comm != NULL: the counts are then summed over the ranks in place (NCCL
+ * all-reduce on `stream`), so every rank holds the global counts; comm == NULL: this
+ * rank's counts only (the caller sums them, e.g. with the page-compact exchange below). */
+edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, edkm_comm* comm,
+                          void* stream);
 
 /* F1 fused with the cross-rank sum of the counts over NVLink SHARP (NVLS) -- the in-kernel
  * form of the integer all-reduce after edkm_uniquify (P:79 learners).
@@ -195,14 +206,16 @@ edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_para
                              void* stream);
 
 /* B1 -- gradient buckets and this rank's partial of gamma_T (DESIGN App. A):
- *   B[u] = sum_{i in slice, bits(w_i)=u} G_i  (64-bit fixed point per CTA, fp64 across CTAs)
+ *   B[u] = sum_{i in slice, bits(w_i)=u} G_i  (exact 32-bit fixed point per CTA in two banks,
+ *          DESIGN S4 "B1"; fp64 across CTAs)
  *   gamma[t*k + l] = sum_u B[u] A_T[u][l] (1 + (C_T[l] - W~_u) 2(v_u - C_T[l]) / tau)
  *   grads[t] : n_t elements, gdtype = weights' 16-bit dtype or FP32.
- *   gamma    : [nt][k] fp64, overwritten.  With several ranks the caller sums gamma
- *              over ranks before edkm_backward_apply. */
+ *   gamma    : [nt][k] fp64, overwritten.  comm != NULL: summed over the ranks in place (NCCL
+ *              all-reduce, bit-identical on every rank); comm == NULL: this rank's partial
+ *              (the caller sums it over ranks before edkm_backward_apply). */
 edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_params* p,
                                  const void* const* grads, int gdtype, const int32_t* counts,
-                                 const void* saved, void* ws, double* gamma, void* stream);
+                                 const void* saved, void* ws, double* gamma, edkm_comm* comm, void* stream);
 
 /* TB + B2 -- reverse loop on the table and dW (DESIGN App. A):
  *   dW_i = G_i phi[u_i] + psi[u_i];  dC0[t*k + l] = dL/dC_0 (fp32, identical on all ranks).
@@ -239,6 +252,45 @@ edkm_status edkm_backward_table_range(int nt, int t0, int t1, const edkm_params*
 edkm_status edkm_backward(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
                           int gdtype, const int32_t* counts, const void* saved, void* ws, void* const* dW,
                           int dw_dtype, float* dC0, void* stream);
+
+/* ---- the communicator (P:79 learners) --------------------------------------
+ *   edkm_comm_unique_id : rank 0 -- writes the 128-byte NCCL unique id to host memory id_out;
+ *                         the caller broadcasts it to the other ranks (e.g. torch.distributed).
+ *   edkm_comm_init      : every rank (collective, blocking) -- a communicator of nranks GPUs on
+ *                         the calling thread's current CUDA device.  *out = NULL on failure.
+ *   edkm_comm_destroy   : every rank, after its last collective (NULL: no-op).
+ *   edkm_comm_info      : rank, nranks, and the NCCL version code of the loaded library.
+ * NCCL (libnccl.so.2) is loaded on first use; if it cannot be, these return EDKM_E_NCCL. */
+edkm_status edkm_comm_unique_id(void* id_out);
+edkm_status edkm_comm_init(edkm_comm** out, const void* id, int rank, int nranks);
+edkm_status edkm_comm_destroy(edkm_comm* comm);
+edkm_status edkm_comm_info(const edkm_comm* comm, int* rank, int* nranks, int* nccl_version);
+
+/* In-place all-reduce of `count` elements of dtype (EDKM_I32, EDKM_FP64, EDKM_FP32, EDKM_U8) with
+ * op EDKM_SUM or EDKM_MAX, on `stream`; and the all-gather of bytes_per_rank bytes from every rank
+ * into recv ([nranks][bytes_per_rank], rank order; send may alias recv's own block).  The
+ * exchanges of the sharded step that the caller composes itself: the page-compact count exchange
+ * below, and the per-tensor blocks of a table phase split by tensor (edkm_forward_range). */
+edkm_status edkm_comm_allreduce(edkm_comm* comm, void* buf, size_t count, int dtype, int op, void* stream);
+edkm_status edkm_comm_allgather(edkm_comm* comm, const void* send, void* recv, size_t bytes_per_rank,
+                                void* stream);
+
+/* ---- page-compact count exchange -----------------------------------------
+ * Page g = t*256 + p is patterns [p*256, p*256+256) of tensor t's counts row.  A rank's counts
+ * are nonzero only on the pages its weights populate (bf16 N(0, 0.02^2): ~30 of 256), so the
+ * ranks sum only the pages SOME rank populated:
+ *   1. edkm_count_pages : mask[g] = 1 if page g of counts has a nonzero entry, else 0 (uint8,
+ *                         [nt][256]); then all-reduce mask with EDKM_MAX;
+ *   2. the caller lists the pages g with mask[g] = 1 (int32 device array `pages`, npages);
+ *   3. edkm_counts_pack : compact[i][0..256) = counts page pages[i];  all-reduce compact (SUM);
+ *   4. edkm_counts_unpack : counts page pages[i] = compact[i].
+ * Pages outside the union are zero on every rank, so counts end up global and exact.  Page ids
+ * outside [0, 256 nt) are skipped.  EDKM_E_ARG for npages outside [0, 256 nt] or NULL buffers. */
+edkm_status edkm_count_pages(const int32_t* counts, int nt, uint8_t* mask, void* stream);
+edkm_status edkm_counts_pack(const int32_t* counts, int nt, const int32_t* pages, int npages, int32_t* compact,
+                             void* stream);
+edkm_status edkm_counts_unpack(const int32_t* compact, const int32_t* pages, int npages, int nt, int32_t* counts,
+                               void* stream);
 
 /* Copies per-tensor status to host and synchronises `stream`:
  *   nonfinite_host[t] = number of weights of tensor t whose pattern is NaN/Inf (global),

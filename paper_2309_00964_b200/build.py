@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "stream_kernels.cu", "table_kernels.cu", "table_wide.cu", "nvls.cu"]
+SOURCES = ["api.cu", "stream_kernels.cu", "table_kernels.cu", "table_wide.cu", "nvls.cu", "exchange.cu"]
 LIB = os.path.join(HERE, "libedkm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
@@ -27,7 +27,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     """Compile libedkm.so (or, for A/B measurements, a variant at `out` with extra -D defines)."""
     if force or out != LIB or _stale():
         cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-               *[os.path.join(CSRC, s) for s in SOURCES], "-lcudart"]
+               *[os.path.join(CSRC, s) for s in SOURCES], "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

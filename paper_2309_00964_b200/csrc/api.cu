@@ -29,6 +29,19 @@ edkm_status cuda_fail(cudaError_t e, const char* where) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+}  // namespace
+
+namespace edkm {
+edkm_status set_error(edkm_status st, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return st;
+}
+void reset_launches() { g_launches = 0; }
+void add_launches(int n) { g_launches += n; }
+}  // namespace edkm
+
+namespace {
+
 int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -195,7 +208,8 @@ size_t edkm_workspace_bytes(int nt, const edkm_params* p) {
   return ws_layout(nt, 1 << p->bits).total;
 }
 
-edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, void* stream) {
+edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, edkm_comm* comm,
+                          void* stream) {
   g_launches = 0;
   if (wdtype != EDKM_BF16 && wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");
   edkm_status st = check_tensors(tensors, nt);
@@ -210,7 +224,7 @@ edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_
   const int sms = sm_count();
   e = for_groups(tensors, nt, nullptr, nullptr, A, [&](const StreamArgs& a) { return launch_f1(a, counts, sms, s); });
   if (e != cudaSuccess) return cuda_fail(e, "F1 histogram launch");
-  return EDKM_OK;
+  return comm_allreduce_sum(comm, counts, (size_t)nt * kPatterns, 0, s);  // global counts on every rank
 }
 
 edkm_status edkm_nvls_set_timeout(double seconds, int trap) {
@@ -383,7 +397,7 @@ edkm_status edkm_backward_gamma(int nt, const edkm_params* p, const int32_t* cou
 
 edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
                                  int gdtype, const int32_t* counts, const void* saved, void* ws, double* gamma,
-                                 void* stream) {
+                                 edkm_comm* comm, void* stream) {
   edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
   if (st != EDKM_OK) return st;
   if (nt > 0 && (!counts || !gamma)) return fail(EDKM_E_ARG, "NULL buffer");
@@ -391,8 +405,10 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
   if (st != EDKM_OK) return st;
   const int n1 = g_launches;
   st = edkm_backward_gamma(nt, p, counts, saved, ws, gamma, stream);
-  if (st == EDKM_OK) g_launches += n1;
-  return st;
+  if (st != EDKM_OK) return st;
+  g_launches += n1;
+  // gamma_T is linear in the buckets: the sum of the ranks' partials is the global gamma_T
+  return comm_allreduce_sum(comm, gamma, (size_t)nt * (1 << p->bits), 1, (cudaStream_t)stream);
 }
 
 edkm_status edkm_backward_table_range(int nt, int t0, int t1, const edkm_params* p, const int32_t* counts,
@@ -496,7 +512,7 @@ edkm_status edkm_backward(const edkm_tensor* tensors, int nt, const edkm_params*
   if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
   if (nt > 0 && !ws) return fail(EDKM_E_ARG, "NULL workspace");
   double* gamma = nt > 0 ? reinterpret_cast<double*>((unsigned char*)ws + ws_layout(nt, 1 << p->bits).gamma) : nullptr;
-  st = edkm_backward_reduce(tensors, nt, p, grads, gdtype, counts, saved, ws, gamma, stream);
+  st = edkm_backward_reduce(tensors, nt, p, grads, gdtype, counts, saved, ws, gamma, nullptr, stream);
   if (st != EDKM_OK) return st;
   const int n1 = g_launches;
   st = edkm_backward_apply(tensors, nt, p, grads, gdtype, counts, saved, ws, gamma, dW, dw_dtype, dC0, stream);
@@ -543,6 +559,7 @@ const char* edkm_status_string(int status) {
     case EDKM_E_DTYPE: return "EDKM_E_DTYPE: unsupported dtype";
     case EDKM_E_CUDA: return "EDKM_E_CUDA: CUDA error";
     case EDKM_E_UNSUPPORTED: return "EDKM_E_UNSUPPORTED: not implemented in this build";
+    case EDKM_E_NCCL: return "EDKM_E_NCCL: NCCL error";
     default: return "unknown edkm_status";
   }
 }

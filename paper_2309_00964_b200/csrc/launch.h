@@ -3,9 +3,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/edkm.h"
 #include "common.cuh"
 
+typedef struct edkm_comm edkm_comm;
+
 namespace edkm {
+
+// ---- error text / launch count of the calling thread (api.cu), used by every entry point
+edkm_status set_error(edkm_status st, const char* msg);
+void reset_launches();
+void add_launches(int n);
+// in-place sum all-reduce over the library's NCCL communicator (exchange.cu); comm == NULL: no-op
+edkm_status comm_allreduce_sum(edkm_comm* comm, void* buf, size_t count, int fp64, cudaStream_t s);
 
 // ---- per-tensor forward state kept in `saved`
 constexpr int kMaxCluster = 8;

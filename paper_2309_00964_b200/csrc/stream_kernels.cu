@@ -280,6 +280,9 @@ __global__ void f1_nvls_wait_kernel(const uint32_t* flags, int nflags, uint32_t*
       __nanosleep(64);
     }
   }
+  // the counts were written through the multicast address and are read (here and by TF) through
+  // the unicast one: order the aliased accesses after the acquire (virtual aliasing proxy)
+  asm volatile("fence.proxy.alias;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_fail) atomicExch(&g_nvls_failed, 1u);

@@ -18,6 +18,16 @@ reductions into a symmetric buffer, summed by the switch into every rank's copy,
 an in-kernel arrival barrier replaces the collective.  Exchange 2 (fp64) stays an
 NCCL all-reduce, whose result is bit-identical on every rank (in-switch fp64 adds
 would arrive in a different order on each GPU).
+
+Where the collectives run: with `comm` (an edkm.Comm, the NCCL communicator owned by
+libedkm.so) the library does them on the step's stream -- inside
+edkm_uniquify / edkm_backward_reduce, or through edkm_comm_allreduce / _allgather.
+Without it, torch.distributed does (gloo in the CPU tests).
+
+compact_counts=True exchanges only the 256-pattern pages of the counts that some rank
+populated: an all-reduce (MAX) of one byte per page, the host lists
+the union's pages (one device->host read of nt*256 bytes: the step's only host sync),
+then the packed pages are summed (~7 MB instead of 59 MB for CFG3) and unpacked.
 """
 from __future__ import annotations
 
@@ -43,6 +53,33 @@ def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
+
+
+def allreduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place max over ranks (no-op without an initialised process group of size > 1)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
+def union_pages(mask: torch.Tensor) -> torch.Tensor:
+    """Global page ids t*256 + p of the pages set in the all-reduced [nt][256] mask, ascending (int32,
+    on the host: the mask's one device->host read).  Identical on every rank (the mask is)."""
+    return torch.nonzero(mask.reshape(-1).cpu()).reshape(-1).to(torch.int32)
+
+
+def exchange_counts_compact(k, allreduce_sum_fn, allreduce_max_fn):
+    """Sum the ranks' counts over the union of their populated pages only.
+
+    `k` has the Plan interface (counts, count_pages, pack_counts, unpack_counts).  Pages that no rank
+    populated are zero on every rank, so after this every rank holds the exact global counts."""
+    mask = k.count_pages()
+    allreduce_max_fn(mask)
+    pages = union_pages(mask).to(k.counts.device)
+    compact = k.pack_counts(pages)
+    allreduce_sum_fn(compact)
+    k.unpack_counts(pages, compact)
+    return pages.numel()
 
 
 def padded_numels(numels, world: int):
@@ -79,14 +116,23 @@ class ShardedStep:
     """
 
     def __init__(self, kernels, group=None, allreduce=None, nvls=None, shard_table=False, allgather=None,
-                 out_mode="all"):
+                 out_mode="all", comm=None, compact_counts=False):
         self.k = kernels
         self.group = group
-        self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
-        self.allgather = allgather or (lambda t: allgather_blocks(t, self.group))
+        self.comm = comm
+        if comm is not None:
+            self.allreduce = allreduce or (lambda t: comm.allreduce(t))
+            self.allreduce_max = lambda t: comm.allreduce(t, op=1)
+            self.allgather = allgather or (lambda t: comm.allgather_blocks(t))
+        else:
+            self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
+            self.allreduce_max = lambda t: allreduce_max(t, self.group)
+            self.allgather = allgather or (lambda t: allgather_blocks(t, self.group))
         self.nvls = nvls
         self.shard_table = shard_table
         self.out_mode = out_mode
+        self.compact_counts = compact_counts
+        self.pages_exchanged = None  # pages summed by the last compact count exchange
 
     def _block(self):
         P = dist.get_world_size(self.group) if dist.is_initialized() else 1
@@ -99,14 +145,22 @@ class ShardedStep:
     def __call__(self, weights, grads, C0, outs, dW):
         if self.nvls is not None:
             self.k.uniquify_nvls(weights, self.nvls)      # exchange 1 fused into F1 (NVSwitch)
+        elif self.compact_counts:
+            self.k.uniquify(weights)                      # exchange 1, populated pages only
+            self.pages_exchanged = exchange_counts_compact(self.k, self.allreduce, self.allreduce_max)
+        elif self.comm is not None:
+            self.k.uniquify(weights, comm=self.comm)      # exchange 1 inside edkm_uniquify
         else:
             self.k.uniquify(weights)
             self.allreduce(self.k.counts)                 # exchange 1: integer counts
         if not self.shard_table:
             self.k.forward(C0)
             self.k.reconstruct(weights, outs)
-            self.k.backward_reduce(weights, grads)
-            self.allreduce(self.k.gamma)                  # exchange 2: gamma_T partials
+            if self.comm is not None:
+                self.k.backward_reduce(weights, grads, comm=self.comm)  # exchange 2 inside the call
+            else:
+                self.k.backward_reduce(weights, grads)
+                self.allreduce(self.k.gamma)              # exchange 2: gamma_T partials
             self.k.backward_apply(weights, grads, dW)
             return self.k.dC0
         t0, t1 = self._block()

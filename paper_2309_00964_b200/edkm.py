@@ -27,11 +27,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # EDKM_LIB selects another build of the same library (A/B measurements of kernel variants)
 LIB_PATH = os.environ.get("EDKM_LIB") or os.path.join(_HERE, "libedkm.so")
 
-BF16, FP16, FP32, U8 = 0, 1, 2, 3
+BF16, FP16, FP32, U8, I32, FP64 = 0, 1, 2, 3, 4, 5
 SOFT, HARD_VALUE, HARD_INDEX = 0, 1, 2
+SUM, MAX = 0, 1
 PATTERNS = 65536
 
-_DT = {torch.bfloat16: BF16, torch.float16: FP16, torch.float32: FP32, torch.uint8: U8}
+_DT = {torch.bfloat16: BF16, torch.float16: FP16, torch.float32: FP32, torch.uint8: U8, torch.int32: I32,
+       torch.float64: FP64}
 
 
 class EDKMError(RuntimeError):
@@ -71,7 +73,7 @@ def lib():
         sig = {
             "edkm_saved_bytes": ([i32, pp], ctypes.c_size_t),
             "edkm_workspace_bytes": ([i32, pp], ctypes.c_size_t),
-            "edkm_uniquify": ([P, i32, i32, P, P], i32),
+            "edkm_uniquify": ([P, i32, i32, P, P, P], i32),
             "edkm_uniquify_nvls": ([P, i32, i32, ctypes.POINTER(_Nvls), P], i32),
             "edkm_nvls_set_timeout": ([ctypes.c_double, i32], i32),
             "edkm_nvls_failed": ([P], i32),
@@ -80,7 +82,7 @@ def lib():
             "edkm_backward_table_range": ([i32, i32, i32, pp, P, P, P, P, P, P], i32),
             "edkm_layout": ([i32, pp, P, P], i32),
             "edkm_reconstruct": ([P, i32, pp, P, P, P, i32, i32, P, P], i32),
-            "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P], i32),
+            "edkm_backward_reduce": ([P, i32, pp, P, i32, P, P, P, P, P, P], i32),
             "edkm_backward_apply": ([P, i32, pp, P, i32, P, P, P, P, P, i32, P, P], i32),
             "edkm_backward": ([P, i32, pp, P, i32, P, P, P, P, i32, P, P], i32),
             "edkm_backward_buckets": ([P, i32, pp, P, i32, P, P, P], i32),
@@ -98,6 +100,15 @@ def lib():
             "edkm_mc_destroy": ([P], i32),
             "edkm_mc_last_error": ([], ctypes.c_char_p),
             "edkm_set_max_ctas": ([i32], i32),
+            "edkm_comm_unique_id": ([P], i32),
+            "edkm_comm_init": ([P, P, i32, i32], i32),
+            "edkm_comm_destroy": ([P], i32),
+            "edkm_comm_info": ([P, P, P, P], i32),
+            "edkm_comm_allreduce": ([P, P, ctypes.c_size_t, i32, i32, P], i32),
+            "edkm_comm_allgather": ([P, P, P, ctypes.c_size_t, P], i32),
+            "edkm_count_pages": ([P, i32, P, P], i32),
+            "edkm_counts_pack": ([P, i32, P, i32, P, P], i32),
+            "edkm_counts_unpack": ([P, P, i32, i32, P, P], i32),
             "edkm_status_string": ([i32], ctypes.c_char_p),
             "edkm_last_error": ([], ctypes.c_char_p),
         }
@@ -116,7 +127,9 @@ def exported_symbols() -> list:
             "edkm_backward_gamma", "edkm_backward_table", "edkm_backward_dw", "edkm_read_status",
             "edkm_last_launch_count", "edkm_set_max_ctas", "edkm_status_string", "edkm_last_error",
             "edkm_mc_supported", "edkm_mc_create", "edkm_mc_import", "edkm_mc_bytes", "edkm_mc_add_device",
-            "edkm_mc_bind", "edkm_mc_destroy", "edkm_mc_last_error"]
+            "edkm_mc_bind", "edkm_mc_destroy", "edkm_mc_last_error", "edkm_comm_unique_id", "edkm_comm_init",
+            "edkm_comm_destroy", "edkm_comm_info", "edkm_comm_allreduce", "edkm_comm_allgather", "edkm_count_pages",
+            "edkm_counts_pack", "edkm_counts_unpack"]
 
 
 def _check(rc: int, what: str):
@@ -197,6 +210,86 @@ def _ptr_array(ts):
     return arr
 
 
+def _comm(comm):
+    return None if comm is None else comm.handle
+
+
+class Comm:
+    """The library's NCCL communicator of the learners (edkm_comm): one per rank, on the current
+    CUDA device.  Rank 0 draws the NCCL unique id (edkm_comm_unique_id) and the id reaches the other
+    ranks through `torch.distributed` (the only thing it is used for); edkm_comm_init then builds the
+    communicator inside the library, and the library's own calls (uniquify / backward_reduce with
+    comm=, allreduce, allgather) run the collectives on the caller's stream."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _check(lib().edkm_comm_unique_id(uid), "edkm_comm_unique_id")
+        if self.nranks > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            ctypes.memmove(uid, obj[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib().edkm_comm_init(ctypes.byref(h), uid, self.rank, self.nranks), "edkm_comm_init")
+        self.handle = h
+        r, n, v = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().edkm_comm_info(h, ctypes.byref(r), ctypes.byref(n), ctypes.byref(v)), "edkm_comm_info")
+        self.nccl_version = v.value
+        if (r.value, n.value) != (self.rank, self.nranks):
+            raise EDKMError(f"edkm_comm rank/nranks {r.value}/{n.value} != {self.rank}/{self.nranks}")
+
+    def allreduce(self, t: torch.Tensor, op: int = SUM, stream=None) -> torch.Tensor:
+        """In-place all-reduce (SUM or MAX) of a contiguous CUDA tensor (int32, fp64, fp32 or uint8)."""
+        t = _flat(t)
+        _check(lib().edkm_comm_allreduce(self.handle, _ptr(t), t.numel(), _DT[t.dtype], op, _stream(stream)),
+               "edkm_comm_allreduce")
+        return t
+
+    def allgather_blocks(self, full: torch.Tensor, stream=None) -> torch.Tensor:
+        """In place: rank r's block is rows [r n/P, (r+1) n/P) of `full`; afterwards every rank has all."""
+        if full.shape[0] % self.nranks:
+            raise EDKMError("allgather_blocks: rows not divisible by the number of ranks")
+        b = full.shape[0] // self.nranks
+        nb = full[0:b].numel() * full.element_size()
+        if not full.is_contiguous():
+            raise EDKMError("allgather_blocks needs a contiguous tensor")
+        send = ctypes.c_void_p(full.data_ptr() + self.rank * nb)
+        _check(lib().edkm_comm_allgather(self.handle, send, _ptr(full), nb, _stream(stream)), "edkm_comm_allgather")
+        return full
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            torch.cuda.synchronize()
+            _check(lib().edkm_comm_destroy(self.handle), "edkm_comm_destroy")
+            self.handle = None
+
+
+def count_pages(counts: torch.Tensor, mask: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """uint8 [nt][256]: 1 where a 256-pattern page of counts has a nonzero entry (edkm_count_pages)."""
+    nt = counts.shape[0]
+    mask = torch.empty((nt, 256), dtype=torch.uint8, device=counts.device) if mask is None else mask
+    _check(lib().edkm_count_pages(_ptr(counts), nt, _ptr(mask), _stream(stream)), "edkm_count_pages")
+    return mask
+
+
+def counts_pack(counts: torch.Tensor, pages: torch.Tensor, compact: torch.Tensor, stream=None):
+    """compact[i] = page pages[i] of counts (edkm_counts_pack); pages: int32 global page ids t*256 + p."""
+    _check(lib().edkm_counts_pack(_ptr(counts), counts.shape[0], _ptr(pages), pages.numel(), _ptr(compact),
+                                  _stream(stream)), "edkm_counts_pack")
+    return compact
+
+
+def counts_unpack(compact: torch.Tensor, pages: torch.Tensor, counts: torch.Tensor, stream=None):
+    """page pages[i] of counts = compact[i] (edkm_counts_unpack)."""
+    _check(lib().edkm_counts_unpack(_ptr(compact), _ptr(pages), pages.numel(), counts.shape[0], _ptr(counts),
+                                    _stream(stream)), "edkm_counts_unpack")
+    return counts
+
+
 def saved_bytes(nt: int, p: Params) -> int:
     return lib().edkm_saved_bytes(nt, ctypes.byref(p.c()))
 
@@ -213,7 +306,7 @@ def uniquify(weights, p: Params, counts: torch.Tensor | None = None, stream=None
             raise EDKMError("all weights must have the params' dtype")
     if counts is None:
         counts = torch.empty((len(ws), PATTERNS), dtype=torch.int32, device=ws[0].device if ws else "cuda")
-    _check(lib().edkm_uniquify(_tensor_array(ws), len(ws), _DT[p.wdtype], _ptr(counts), _stream(stream)),
+    _check(lib().edkm_uniquify(_tensor_array(ws), len(ws), _DT[p.wdtype], _ptr(counts), None, _stream(stream)),
            "edkm_uniquify")
     return counts
 
@@ -252,7 +345,7 @@ def backward_reduce(weights, grads, p: Params, counts, saved, ws_buf, gamma=None
     gdt = _DT[gs[0].dtype] if gs else _DT[p.wdtype]
     gamma = torch.empty((len(ws), p.k), dtype=torch.float64, device=counts.device) if gamma is None else gamma
     _check(lib().edkm_backward_reduce(_tensor_array(ws), len(ws), ctypes.byref(p.c()), _ptr_array(gs), gdt,
-                                      _ptr(counts), _ptr(saved), _ptr(ws_buf), _ptr(gamma), _stream(stream)),
+                                      _ptr(counts), _ptr(saved), _ptr(ws_buf), _ptr(gamma), None, _stream(stream)),
            "edkm_backward_reduce")
     return gamma
 
@@ -319,6 +412,15 @@ class Plan:
         self.dC0 = torch.empty((self.nt, p.k), dtype=torch.float32, device=dev)
         self._cache = {}
 
+    def _n(self, tensors, what):
+        """Every list a Plan call passes to the C ABI holds exactly nt tensors of the planned sizes:
+        a shorter list would make the library read past the host array."""
+        if len(tensors) != self.nt:
+            raise EDKMError(f"{what}: {len(tensors)} tensors, the plan has {self.nt}")
+        for t, n in zip(tensors, self.numels):
+            if t.numel() != n:
+                raise EDKMError(f"{what}: a tensor of {t.numel()} elements where the plan has {n}")
+
     def _arr(self, key, tensors, maker):
         ptrs = tuple(t.data_ptr() for t in tensors)
         hit = self._cache.get(key)
@@ -327,19 +429,39 @@ class Plan:
             self._cache[key] = hit
         return hit[1]
 
-    def uniquify(self, weights, stream=None):
+    def uniquify(self, weights, stream=None, comm=None):
+        """F1; with `comm` (a Comm) the counts are summed over the ranks inside the call."""
+        self._n(weights, "weights")
         _check(lib().edkm_uniquify(self._arr("w", weights, _tensor_array), self.nt, _DT[self.p.wdtype],
-                                   _ptr(self.counts), _stream(stream)), "edkm_uniquify")
+                                   _ptr(self.counts), _comm(comm), _stream(stream)), "edkm_uniquify")
         return self.counts
 
     def uniquify_nvls(self, weights, nvls, stream=None):
         """F1 with the cross-rank count sum done in the NVSwitch (edkm_uniquify_nvls); `nvls` is a
         dist.NvlsCounts.  Leaves self.counts = this step's local view of the global counts."""
-        x = nvls.next_step()
+        self._n(weights, "weights")
+        x = nvls.next_step(stream)
         _check(lib().edkm_uniquify_nvls(self._arr("w", weights, _tensor_array), self.nt, _DT[self.p.wdtype],
                                         ctypes.byref(x), _stream(stream)), "edkm_uniquify_nvls")
         self.counts = nvls.current
         return self.counts
+
+    # the page-compact count exchange (include/edkm.h; dist.ShardedStep(compact_counts=True))
+    def count_pages(self, stream=None):
+        """uint8 [nt][256]: pages of this rank's counts with a nonzero entry (edkm_count_pages)."""
+        if getattr(self, "_mask", None) is None:
+            self._mask = torch.empty((max(self.nt, 1), 256), dtype=torch.uint8, device=self.counts.device)
+        return count_pages(self.counts, self._mask[:self.nt], stream)
+
+    def pack_counts(self, pages: torch.Tensor, stream=None) -> torch.Tensor:
+        """int32 [len(pages)][256]: the listed pages of the counts, in list order (edkm_counts_pack)."""
+        if getattr(self, "_compact", None) is None:
+            self._compact = torch.empty((max(self.nt, 1) * 256, 256), dtype=torch.int32, device=self.counts.device)
+        return counts_pack(self.counts, pages, self._compact[:pages.numel()], stream)
+
+    def unpack_counts(self, pages: torch.Tensor, compact: torch.Tensor, stream=None):
+        """The listed pages of the counts = compact (edkm_counts_unpack)."""
+        return counts_unpack(compact, pages, self.counts, stream)
 
     def forward(self, C0, stream=None):
         _check(lib().edkm_forward(_ptr(self.counts), self.nt, ctypes.byref(self.p.c()), _ptr(C0), _ptr(self.C_out),
@@ -387,22 +509,29 @@ class Plan:
         return self._views
 
     def reconstruct(self, weights, outs, mode=SOFT, stream=None):
+        self._n(weights, "weights")
+        self._n(outs, "outs")
         odt = _DT[outs[0].dtype] if outs else _DT[self.p.wdtype]
         _check(lib().edkm_reconstruct(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
                                       _ptr(self.table), _ptr(self.C_out), _ptr(self.saved), mode, odt,
                                       self._arr(("o", mode), outs, _ptr_array), _stream(stream)), "edkm_reconstruct")
         return outs
 
-    def backward_reduce(self, weights, grads, stream=None):
+    def backward_reduce(self, weights, grads, stream=None, comm=None):
+        """B1 + TGAMMA; with `comm` gamma_T is summed over the ranks inside the call."""
+        self._n(weights, "weights")
+        self._n(grads, "grads")
         gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
         _check(lib().edkm_backward_reduce(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
                                           self._arr("g", grads, _ptr_array), gdt, _ptr(self.counts),
-                                          _ptr(self.saved), _ptr(self.ws), _ptr(self.gamma), _stream(stream)),
-               "edkm_backward_reduce")
+                                          _ptr(self.saved), _ptr(self.ws), _ptr(self.gamma), _comm(comm),
+                                          _stream(stream)), "edkm_backward_reduce")
         return self.gamma
 
     # the four backward kernels individually (B1, TGAMMA, TB, B2)
     def backward_buckets(self, weights, grads, stream=None):
+        self._n(weights, "weights")
+        self._n(grads, "grads")
         gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
         _check(lib().edkm_backward_buckets(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
                                            self._arr("g", grads, _ptr_array), gdt, _ptr(self.saved), _ptr(self.ws),
@@ -420,6 +549,9 @@ class Plan:
         return self.dC0
 
     def backward_dw(self, weights, grads, dW, stream=None):
+        self._n(weights, "weights")
+        self._n(grads, "grads")
+        self._n(dW, "dW")
         gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
         ddt = _DT[dW[0].dtype] if dW else _DT[self.p.wdtype]
         _check(lib().edkm_backward_dw(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
@@ -428,6 +560,9 @@ class Plan:
         return dW
 
     def backward_apply(self, weights, grads, dW, stream=None):
+        self._n(weights, "weights")
+        self._n(grads, "grads")
+        self._n(dW, "dW")
         gdt = _DT[grads[0].dtype] if grads else _DT[self.p.wdtype]
         ddt = _DT[dW[0].dtype] if dW else _DT[self.p.wdtype]
         _check(lib().edkm_backward_apply(self._arr("w", weights, _tensor_array), self.nt, ctypes.byref(self.p.c()),
@@ -480,6 +615,7 @@ class EDKMFunction(torch.autograd.Function):
         C_out, table, saved = forward(counts, C0.detach().reshape(1, -1), p)
         (Wt,) = reconstruct([w], p, table, C_out, saved, SOFT, W.dtype)
         ctx.p = p
+        ctx.C0_shape, ctx.C0_dtype = C0.shape, C0.dtype  # dC0 is returned in C0's shape and dtype
         ctx.save_for_backward(w, counts, saved)
         return Wt.view_as(W)
 
@@ -490,7 +626,7 @@ class EDKMFunction(torch.autograd.Function):
         if g.dtype not in (ctx.p.wdtype, torch.float32):
             g = g.float()
         (dW,), dC0 = backward([w], [g], ctx.p, counts, saved, dw_dtype=w.dtype)
-        return dW.view_as(w), dC0.reshape(-1), None
+        return dW.view_as(w), dC0.reshape(ctx.C0_shape).to(ctx.C0_dtype), None
 
 
 def edkm(W: torch.Tensor, C0: torch.Tensor, bits: int = 3, tau: float = 1e-3, max_iter: int = 5, eps: float = 0.0):

@@ -40,14 +40,14 @@ def test_every_declared_symbol_is_exported(L):
 def test_bad_arguments_return_errors_without_launch(L):
     p = E.Params()
     cp = ctypes.byref(p.c())
-    assert L.edkm_uniquify(None, -1, 0, None, None) == 1
-    assert L.edkm_uniquify(None, 1, 0, None, None) == 1           # NULL tensors
-    assert L.edkm_uniquify(None, 0, 7, None, None) == 2           # bad dtype
+    assert L.edkm_uniquify(None, -1, 0, None, None, None) == 1
+    assert L.edkm_uniquify(None, 1, 0, None, None, None) == 1           # NULL tensors
+    assert L.edkm_uniquify(None, 0, 7, None, None, None) == 2           # bad dtype
     t = (E._Tensor * 1)()
     t[0].w, t[0].n = None, 5
-    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None) == 1   # n > 0 with NULL data
+    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None, None) == 1   # n > 0 with NULL data
     t[0].w, t[0].n = 3, 5
-    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None) == 1   # odd address
+    assert L.edkm_uniquify(t, 1, 0, ctypes.c_void_p(16), None, None) == 1   # odd address
     for bad in (E._Params(0, 3, -1.0, 5, 0.0), E._Params(0, 3, float("nan"), 5, 0.0), E._Params(0, 3, 1.0, -1, 0.0),
                 E._Params(0, 3, 1.0, 5, -1.0), E._Params(0, 3, float("inf"), 5, 0.0)):
         assert L.edkm_forward(ctypes.c_void_p(16), 1, ctypes.byref(bad), ctypes.c_void_p(16), ctypes.c_void_p(16),
@@ -65,10 +65,31 @@ def test_bad_arguments_return_errors_without_launch(L):
     assert L.edkm_status_string(0) == b"EDKM_OK"
 
 
+def test_comm_and_exchange_arguments(L):
+    """the communicator behind the ABI and the page-compact exchange reject bad arguments
+    synchronously (nothing launched, no NCCL call), and EDKM_E_NCCL exists."""
+    h = ctypes.c_void_p(1)
+    assert L.edkm_comm_init(None, None, 0, 1) == 1
+    uid = (ctypes.c_uint8 * 128)()
+    assert L.edkm_comm_init(ctypes.byref(h), uid, 1, 1) == 1 and h.value is None   # rank outside [0, nranks)
+    assert L.edkm_comm_init(ctypes.byref(h), uid, 0, 0) == 1                       # nranks < 1
+    assert L.edkm_comm_unique_id(None) in (1, 5)
+    assert L.edkm_comm_destroy(None) == 0
+    assert L.edkm_comm_allreduce(None, None, 0, E.I32, E.SUM, None) == 1
+    assert L.edkm_comm_allgather(None, None, None, 0, None) == 1
+    assert L.edkm_count_pages(None, -1, None, None) == 1
+    assert L.edkm_count_pages(None, 0, None, None) == 0
+    assert L.edkm_count_pages(None, 2, None, None) == 1
+    assert L.edkm_counts_pack(None, 1, None, 257, None, None) == 1                 # npages > 256 nt
+    assert L.edkm_counts_pack(None, 1, None, 0, None, None) == 0
+    assert L.edkm_counts_unpack(None, None, 3, 1, None, None) == 1
+    assert L.edkm_status_string(5).startswith(b"EDKM_E_NCCL")
+
+
 def test_empty_calls_are_noops(L):
     p = E.Params()
     cp = ctypes.byref(p.c())
-    assert L.edkm_uniquify(None, 0, 0, None, None) == 0
+    assert L.edkm_uniquify(None, 0, 0, None, None, None) == 0
     assert L.edkm_forward(None, 0, cp, None, None, None, None, None) == 0
     assert L.edkm_backward(None, 0, cp, None, 0, None, None, None, None, 0, None, None) == 0
 

@@ -40,6 +40,16 @@ class OracleKernels:
         for t, w in enumerate(weights):
             self.counts[t] = torch.from_numpy(O.histogram(self.bits(w)).astype(np.int32))
 
+    # page-compact count exchange (stand-ins of edkm_count_pages / _counts_pack / _counts_unpack)
+    def count_pages(self):
+        return (self.counts.reshape(self.nt, 256, 256) != 0).any(dim=2).to(torch.uint8)
+
+    def pack_counts(self, pages):
+        return self.counts.reshape(-1, 256)[pages.long()].clone()
+
+    def unpack_counts(self, pages, compact):
+        self.counts.reshape(-1, 256)[pages.long()] = compact
+
     def _uniq(self, t):
         u = np.nonzero(self.counts[t].numpy())[0]
         v = O.decode16(u.astype(np.uint16), O.BF16)
@@ -99,6 +109,62 @@ def _worker(rank, world, port, q):
                [tr[0] for tr in kern.traj], kern.counts.numpy().sum(1)))
     finally:
         dist.destroy_process_group()
+
+
+def _compact_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_00964_b200.dist import exchange_counts_compact, allreduce_max, allreduce_sum
+        sizes, Ws = compact_inputs()
+        rng = shard_all(sizes, rank, world)
+        kern = OracleKernels(len(sizes), K)
+        kern.uniquify([w[a:b].contiguous() for w, (a, b) in zip(Ws, rng)])
+        local_pages = int(kern.count_pages().sum())
+        npages = exchange_counts_compact(kern, allreduce_sum, allreduce_max)
+        q.put((rank, kern.counts.numpy().copy(), npages, local_pages))
+    finally:
+        dist.destroy_process_group()
+
+
+def compact_inputs():
+    # rank-disjoint page sets (tensor 1: positive weights in the first half, negative in the second),
+    # a tensor only one rank populates, an empty tensor, and a tiny one
+    sizes = [50_000, 40_000, 0, 3, 1]
+    Ws = [synth.normal_tensor(sizes[0], 0.02, torch.bfloat16, 901)]
+    x = synth.normal_tensor(sizes[1], 1.0, torch.bfloat16, 902).abs()
+    Ws.append(torch.cat([x[:20_000], -x[20_000:]]))
+    Ws += [torch.zeros(0, dtype=torch.bfloat16), synth.normal_tensor(3, 1.0, torch.bfloat16, 903),
+           torch.tensor([1e-30], dtype=torch.bfloat16)]
+    return sizes, Ws
+
+
+def test_world_size_2_gloo_compact_count_exchange_matches_oracle_histogram():
+    """dist.exchange_counts_compact: every rank ends with the exact global counts of
+    every tensor (O.histogram of the whole tensor) although only the union of the ranks' populated pages
+    was summed."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_compact_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=300)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sizes, Ws = compact_inputs()
+    for r in range(world):
+        for t, w in enumerate(Ws):
+            ref = O.histogram(w.view(torch.int16).numpy().view(np.uint16))
+            np.testing.assert_array_equal(res[r][1][t], ref.astype(np.int32))
+    assert res[0][2] == res[1][2] < len(sizes) * 256            # same union on both ranks, compact
+    assert res[0][2] >= max(res[0][3], res[1][3])               # it covers each rank's own pages
+    assert res[0][2] < res[0][3] + res[1][3]                    # pages shared by both are summed once
 
 
 def free_port():

@@ -191,3 +191,64 @@ def test_nvls_fused_counts_world1(emulate):
     assert epoch == 6  # five uniquify_nvls steps + the ShardedStep
     if emulate:
         assert timeout_ok  # non-trapping timeout recorded once (edkm_nvls_set_timeout / edkm_nvls_failed)
+
+
+def _comm_worker(q, compact):
+    """The sharded step with every collective inside libedkm.so: edkm_comm_init at
+    nranks = 1 on the one B200, then ShardedStep(comm=...) -- counts summed inside edkm_uniquify (or by
+    the page-compact exchange through edkm_comm_allreduce), gamma_T inside edkm_backward_reduce."""
+    from paper_2309_00964_b200.dist import ShardedStep as SS
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    comm = E.Comm()
+    try:
+        p = E.Params(torch.bfloat16, **P_)
+        Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i).to(dev) for i, n in enumerate(SIZES)]
+        Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i).to(dev) for i, n in enumerate(SIZES)]
+        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
+        plan = E.Plan(SIZES, p, dev)
+        outs = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        dW = [torch.empty(n, dtype=torch.float32, device=dev) for n in SIZES]
+        step = SS(plan, comm=comm, compact_counts=compact)
+        for _ in range(2):  # twice: the step reuses every buffer
+            step(Ws, Gs, C0, outs, dW)
+        torch.cuda.synchronize()
+        q.put(("ok", comm.nranks, comm.nccl_version, step.pages_exchanged, plan.counts.cpu().numpy(),
+               plan.C_out.cpu().numpy(), plan.dC0.cpu().numpy(), [o.cpu().double().numpy() for o in outs],
+               [d.cpu().double().numpy() for d in dW]))
+    except Exception as e:  # report to the parent instead of hanging it
+        q.put(("err", repr(e)))
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("compact", [False, True])
+def test_comm_in_the_c_abi_nranks1_matches_oracle(compact):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_comm_worker, args=(q, compact))
+    pr.start()
+    out = q.get(timeout=600)
+    pr.join(timeout=120)
+    assert out[0] == "ok", out
+    _, nranks, version, npages, counts, C, dC0, outs, dWs = out
+    assert nranks == 1 and version >= 22700
+    k = 1 << P_["bits"]
+    C0 = np.float32(synth.quantile_centroids(k, 1.0)).astype(np.float64)
+    pages = 0
+    for t, n in enumerate(SIZES):
+        W = synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + t)
+        G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + t)
+        bits = W.view(torch.int16).numpy().view(np.uint16)
+        c = O.histogram(bits)
+        assert np.array_equal(counts[t], c.astype(np.int32))
+        pages += int(np.any(c.reshape(256, 256) != 0, axis=1).sum())
+        w = O.decode16(bits, O.BF16)
+        Ct, St, _ = O.dkm_forward(w, C0, P_["tau"], P_["max_iter"])
+        Wt = O.reconstruct(w, Ct[-1], P_["tau"])
+        dWr, dC = O.dkm_backward(w, G.double().numpy(), Ct, St, P_["tau"])
+        assert np.max(np.abs(C[t] - Ct[-1])) <= TOL * np.max(np.abs(Ct[-1]))
+        assert np.max(np.abs(dC0[t] - dC)) <= TOL * np.max(np.abs(dC))
+        assert np.max(np.abs(outs[t] - Wt)) <= TOL * np.max(np.abs(Wt))
+        assert np.max(np.abs(dWs[t] - dWr)) <= TOL * np.max(np.abs(dWr))
+    assert npages == (pages if compact else None)
