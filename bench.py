@@ -126,9 +126,9 @@ def oracle_sample_step(w_bits, G, C0, wl, nthreads):
     dt = O.BF16 if str(wl.wdtype).endswith("bfloat16") else O.FP16
     w = O.decode16(w_bits, dt)
     Ct, St, T = O.dkm_forward(w, np.float32(C0).astype(np.float64), wl.tau, wl.max_iter, nthreads=nthreads)
-    O.reconstruct(w, Ct[-1], wl.tau)
-    O.dkm_backward(w, G, Ct, St, wl.tau, nthreads=nthreads)
-    return w.size
+    Wt = O.reconstruct(w, Ct[-1], wl.tau)
+    dW, dC = O.dkm_backward(w, G, Ct, St, wl.tau, nthreads=nthreads)
+    return w.size, (Ct[-1], Wt, dW, dC)
 
 
 def cpu_sample(wl, n_target, seed_t=1):
@@ -152,22 +152,55 @@ def calibrate_cpu(wl, seconds, nthreads):
     return max(n0, int(n0 * seconds / max(dt, 1e-6)))
 
 
-def cpu_baseline(wl, seconds):
-    """Dense oracle over whole tensors of layer 0 (q, k, v, ...) in order until ~`seconds` elapse."""
+def cpu_baseline(wl, seconds, gpu_result=None, fetch=None):
+    """Dense oracle over whole tensors of layer 0 (q, k, v, ...) in order until ~`seconds` elapse, on
+    every host core; then the same oracle on ONE thread over a 1M-weight sample.  `gpu_result(t)` gives
+    the bench step's own outputs for tensor t (C_T, dC_0 and this rank's slice of W~, dW); they are
+    compared with the oracle's outputs for the tensors timed here (untimed), as the line's parity.
+    `fetch(t)` gives the bench's own (W bits, G) of the whole tensor t (else the same law on the CPU)."""
+    import numpy as np
     cores = len(os.sched_getaffinity(0))
-    done, names, t0 = 0, [], time.perf_counter()
+    done, names, refs, tt = 0, [], {}, 0.0
     for t in range(1, len(wl.shapes)):
         n = wl.shapes[t][1] * wl.shapes[t][2]
         b, G, C0 = cpu_sample(wl, n, seed_t=t)
-        oracle_sample_step(b, G, C0, wl, cores)
+        if fetch is not None:
+            b, G = fetch(t)
+        t0 = time.perf_counter()
+        _, refs[t] = oracle_sample_step(b, G, C0, wl, cores)
+        tt += time.perf_counter() - t0
         done += b.size
         names.append(wl.shapes[t][0])
-        if time.perf_counter() - t0 >= seconds:
+        if tt >= seconds:
             break
-    dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "weights/s", "cores": cores, "kind": "oracle",
-            "sample": f"dense fp64 oracle fwd+bwd (all |W|x|C| entries, T={wl.max_iter}, k={wl.k}, tau={wl.tau}) "
-                      f"on whole tensors {names} ({done} weights, {wl.name} law), {dt:.1f} s on {cores} threads"}
+    dt = tt
+    b1, G1, C01 = cpu_sample(wl, 1 << 20, seed_t=1)
+    t1 = time.perf_counter()
+    oracle_sample_step(b1, G1, C01, wl, 1)
+    dt1 = time.perf_counter() - t1
+    out = {"value": done / dt, "unit": "weights/s", "cores": cores, "kind": "oracle",
+           "sample": f"dense fp64 oracle fwd+bwd (all |W|x|C| entries, T={wl.max_iter}, k={wl.k}, tau={wl.tau}) "
+                     f"on whole tensors {names} ({done} weights, {wl.name} law), {dt:.1f} s on {cores} threads",
+           "value_1thread": b1.size / dt1,
+           "sample_1thread": f"the same oracle on 1 thread, first {b1.size} weights of {wl.shapes[1][0]}, {dt1:.1f} s"}
+    if gpu_result is not None:
+        def nw(a, r):
+            a, r = np.asarray(a, np.float64), np.asarray(r, np.float64)
+            return float(np.max(np.abs(a - r)) / max(np.max(np.abs(r)), 1e-300)) if r.size else 0.0
+        par = {"tensors": names, "C_T": 0.0, "dC0": 0.0, "W~": 0.0, "dW": 0.0}
+        for t, (CT, Wt, dW, dC) in refs.items():
+            g = gpu_result(t)
+            lo, hi = g["slice"]
+            par["C_T"] = max(par["C_T"], nw(g["C"], CT))
+            par["dC0"] = max(par["dC0"], nw(g["dC0"], dC))
+            # 16-bit outputs: normwise against the fp64 oracle (includes the bf16 rounding, ~2^-9)
+            par["W~"] = max(par["W~"], nw(g["Wt"], Wt[lo:hi]))
+            par["dW"] = max(par["dW"], nw(g["dW"], dW[lo:hi]))
+        par["note"] = ("normwise max|x - x_ref| / max|x_ref| of the step's own outputs vs the dense oracle on the "
+                       "tensors above; C_T, dC_0 fp32 (bar 1e-5), W~ and dW are the bf16/fp16 outputs (their "
+                       "rounding, up to 2^-8 / 2^-11 relative, included)")
+        out["parity"] = par
+    return out
 
 
 def run_reference(args):
@@ -209,7 +242,7 @@ def main():
     from paper_2309_00964_b200 import build as B
     from paper_2309_00964_b200 import edkm as E
     from paper_2309_00964_b200 import synth
-    from paper_2309_00964_b200.dist import shard_range
+    from paper_2309_00964_b200.dist import exchange_counts_compact, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -224,6 +257,9 @@ def main():
     if distributed:
         torch.cuda.set_device(local)
         if backend == "nccl":
+            # NCCL's init lines (rank, nRanks, transports) stay visible on stderr at N > 1
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -266,18 +302,31 @@ def main():
     views = plan.views() if shard else None
     stream = torch.cuda.current_stream()
 
+    # N > 1 collectives: by default on libedkm.so's own NCCL communicator (edkm.Comm, SURVEY S8(b):
+    # edkm_comm_allreduce / _allgather on the step's stream); EDKM_COMM=torch uses torch.distributed
+    comm = None
+    if distributed and backend == "nccl" and os.environ.get("EDKM_COMM", "lib") == "lib":
+        comm = E.Comm()
+
     def allreduce(t, op=None):
         op = dist.ReduceOp.SUM if op is None else op
         if not distributed:
             return
-        if backend == "nccl":
+        if comm is not None:
+            comm.allreduce(t, op=E.MAX if op == dist.ReduceOp.MAX else E.SUM)
+        elif backend == "nccl":
             dist.all_reduce(t, op=op)
         else:  # gloo check mode: through host memory
             h = t.cpu()
             dist.all_reduce(h, op=op)
             t.copy_(h)
 
+    def allreduce_max(t):
+        allreduce(t, op=dist.ReduceOp.MAX)
+
     def allgather(full):
+        if comm is not None:
+            return comm.allgather_blocks(full)
         if backend == "nccl":
             return allgather_blocks(full)
         P = dist.get_world_size()  # gloo check mode: rank blocks through host memory
@@ -289,8 +338,15 @@ def main():
 
     # N > 1: exchange 1 fused into F1 over NVLS (dist.NvlsCounts) when the system supports it and
     # it passes a bit-exact self-check against F1 + NCCL all-reduce; otherwise NCCL.
-    nv, exchange = None, "nccl all-reduce (counts int32, gamma fp64)"
-    mode = os.environ.get("EDKM_NVLS", "1")
+    # exchange 1: only the populated 256-pattern pages of the counts (dist.exchange_counts_compact,
+    # SURVEY S8(e) #1) unless EDKM_COMPACT=0
+    compact = distributed and os.environ.get("EDKM_COMPACT", "1") == "1"
+    via = "libedkm.so's NCCL comm (edkm_comm_*)" if comm is not None else f"torch.distributed ({backend})"
+    nv, exchange = None, (f"counts: {'page-compact ' if compact else ''}int32 all-reduce; gamma: fp64 all-reduce; "
+                          f"via {via}")
+    # the NVLS-fused count exchange (multimem reductions inside F1) has not yet run on NVSwitch
+    # hardware: opt-in (EDKM_NVLS=1) until it has been validated there
+    mode = os.environ.get("EDKM_NVLS", "0")
     if (world > 1 and mode != "0") or mode == "emulate":  # emulate: the protocol on plain memory, one rank
         from paper_2309_00964_b200.dist import NvlsCounts
         try:
@@ -309,6 +365,9 @@ def main():
             if ok.item() != 1.0:
                 raise RuntimeError("NVLS counts differ from the NCCL all-reduce")
             exchange = "counts: NVLS multimem reductions fused into F1 + in-kernel arrival barrier; gamma: nccl all-reduce"
+            if rank == 0:
+                print(f"bench: NVLS count exchange self-check passed ({'emulate' if mode == 'emulate' else 'multicast'})",
+                      file=sys.stderr)
         except Exception as e:  # no multicast, or a failed self-check: NCCL
             if rank == 0:
                 print(f"bench: NVLS count exchange unavailable ({e}); using NCCL", file=sys.stderr)
@@ -327,7 +386,10 @@ def main():
         else:
             plan.uniquify(Ws)                # F1
             mark(1)
-            allreduce(plan.counts)           # exchange 1 (N > 1)
+            if compact:                      # exchange 1 (N > 1), populated pages only
+                exchange_counts_compact(plan, allreduce, allreduce_max)
+            else:
+                allreduce(plan.counts)       # exchange 1 (N > 1)
         mark(2)
         if shard:
             plan.forward_range(t0, t1, C0)   # TF, this rank's tensor block
@@ -379,7 +441,25 @@ def main():
     if distributed:
         allreduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    launches_per_step = 7 + (nv is not None)  # + the NVLS arrival-barrier kernel
+    launches_per_step = 7 + (nv is not None) + 3 * (compact and nv is None)  # + NVLS barrier / page exchange
+    # N > 1: C_T and dC_0 must be bit-identical on every rank ("weights are identical in each
+    # learner"): all-gather a hash of their bytes and fail on any mismatch
+    rank_identical = None
+    if distributed:
+        import hashlib
+        hsh = hashlib.sha256(plan.C_out.cpu().numpy().tobytes() + plan.dC0.cpu().numpy().tobytes()).digest()[:8]
+        mine = torch.tensor([int.from_bytes(hsh, "little", signed=True)], dtype=torch.int64)
+        allh = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        if backend == "nccl":
+            got = torch.zeros(world, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(got, mine.to(dev))
+            allh = got.cpu().tolist()
+        else:
+            dist.all_gather(allh, mine)
+            allh = [int(x.item()) for x in allh]
+        rank_identical = len(set(allh)) == 1
+        if not rank_identical:
+            raise RuntimeError(f"C_T / dC_0 differ across ranks (hashes {allh})")
 
     # ---- the same step captured once as a CUDA graph and replayed (Plan.graph; one GPU)
     graph = None
@@ -443,10 +523,13 @@ def main():
         del hW, hG, hWt, hdW
 
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if distributed:
             dist.destroy_process_group()
         return
 
+    w16 = "bf16" if wl.wdtype == torch.bfloat16 else "fp16"
     # ---- roofline of the dominant per-weight kernel (measured live above)
     peak, peak_src = measured_peaks()
     per_kernel = {k: phase[k] for k in ("F1", "F2", "B1", "B2")}
@@ -456,27 +539,42 @@ def main():
     achieved = alg / (per_kernel[dom] / 1e3) / 1e9
     tr = ncu_traffic(key)
     roof = {"bound": "hbm", "kernel": key, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": (tr * n_local if tr is not None else None), "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": alg,
-            "step_frac": (16 * n_local / (ms_max / 1e3) / 1e9) / peak}
+            "traffic": (tr * n_local if tr is not None else None),
+            "traffic_source": "not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum per weight of "
+                              "this kernel from the committed ncu --set full capture (profiles/ncu_full_summary.json) "
+                              "x the weights of one launch",
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+            "frac_of_spec_8tbs": achieved / 8000.0,
+            "step_frac": (16 * n_local / (ms_max / 1e3) / 1e9) / peak,
+            "step_frac_of_spec_8tbs": (16 * n_local / (ms_max / 1e3) / 1e9) / 8000.0}
     out = {
         "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": "weights/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": w16, "data": "synthetic",
         "config": {"workload": f"{wl.name}: LLaMA-7B-shaped, {len(wl.shapes)} tensors, {n_total} weights, "
                                f"{'bf16' if wl.wdtype == torch.bfloat16 else 'fp16'} N(0,{wl.sigma}^2), "
                                f"b={wl.bits} (k={wl.k}), tau={wl.tau}, T={wl.max_iter}",
                    "tensors": len(wl.shapes), "weights": n_total, "bits": wl.bits, "tau": wl.tau,
                    "iters": wl.max_iter, "parallelism": f"slices{world}", "exchange": exchange,
                    "table_phase": "split by tensor block + all-gather" if shard else "replicated on every rank",
-                   "arith": "bf16 I/O; fp32 per-weight passes; fp64 table phase",
+                   "arith": f"{w16} I/O; exact integer F1/B1 sums, fp32 B2 FMA; fp64 table phase",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
-        "phases_ms": phase, "gpu_launches": launches_per_step * args.steps,
+        "phases_ms": phase, "gpu_launches": launches_per_step * args.steps, "rank_identical_C_dC0": rank_identical,
         "clocks": clk.summary(), "roofline": roof, "e2e": e2e, "cuda_graph": graph,
     }
-    if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)
+    if not args.no_cpu_baseline:  # rank 0 (at N > 1 too): the oracle on the host cores + the step's parity
+        def gpu_result(t):
+            lo, hi = shard_range(wl.shapes[t][1] * wl.shapes[t][2], rank, world)
+            return {"C": plan.C_out[t].cpu().numpy(), "dC0": plan.dC0[t].cpu().numpy(), "slice": (lo, hi),
+                    "Wt": Wt[t].double().cpu().numpy(), "dW": dW[t].double().cpu().numpy()}
+        def fetch(t):  # the bench's own data of tensor t, whole (CUDA generator, as above)
+            import numpy as np
+            return (synth.weights(wl, t, dev).cpu().view(torch.int16).numpy().view(np.uint16),
+                    synth.grads(wl, t, dev).double().cpu().numpy())
+        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds, gpu_result, fetch)
     print(json.dumps(out))
+    if comm is not None:
+        comm.close()
     if distributed:
         dist.destroy_process_group()
 

@@ -90,16 +90,18 @@ edkm_status need_nccl() {
 // exchange only the pages some rank populated: an all-reduce (MAX) of one byte per page, then a
 // sum all-reduce of the packed pages (~7 MB instead of 59 MB for CFG3).
 
-// mask[g] = 1 if page g has a nonzero count: one warp per page, 8 counts per lane (two int4)
+// mask[g] = 1 if page g has a nonzero count: one warp per page, 8 counts per lane (two int4),
+// grid-stride over the pages
 __global__ void count_pages_kernel(const int32_t* __restrict__ counts, int64_t npages, uint8_t* __restrict__ mask) {
-  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t wpb = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= npages) return;
-  const int4* p = reinterpret_cast<const int4*>(counts + warp * 256) + lane * 2;
-  const int4 a = __ldg(p), b = __ldg(p + 1);
-  const int any = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0;
-  const unsigned m = __ballot_sync(0xffffffffu, any);
-  if (lane == 0) mask[warp] = m != 0;
+  for (int64_t g = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); g < npages; g += (int64_t)gridDim.x * wpb) {
+    const int4* p = reinterpret_cast<const int4*>(counts + g * 256) + lane * 2;
+    const int4 a = __ldg(p), b = __ldg(p + 1);
+    const int any = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, any);
+    if (lane == 0) mask[g] = m != 0;
+  }
 }
 
 // DIR 0: compact[i] = counts page pages[i]; DIR 1: counts page pages[i] = compact[i].

@@ -252,3 +252,28 @@ def test_comm_in_the_c_abi_nranks1_matches_oracle(compact):
         assert np.max(np.abs(outs[t] - Wt)) <= TOL * np.max(np.abs(Wt))
         assert np.max(np.abs(dWs[t] - dWr)) <= TOL * np.max(np.abs(dWr))
     assert npages == (pages if compact else None)
+
+
+@pytest.mark.parametrize("nt", [1, 226, 600])
+def test_page_exchange_kernels(nt):
+    """edkm_count_pages / _counts_pack / _counts_unpack at up to 600 x 256 pages (more than one grid of
+    the kernels) against their plain definitions: a page is populated iff any of its 256 counts is
+    nonzero; pack gathers the listed pages in list order; unpack scatters them back."""
+    g = torch.Generator().manual_seed(nt)
+    counts = torch.zeros((nt, 65536), dtype=torch.int32)
+    pages = torch.randperm(nt * 256, generator=g)[: max(1, nt * 256 // 7)]
+    for pg in pages.tolist():
+        counts.view(-1, 256)[pg, int(torch.randint(0, 256, (1,), generator=g))] = int(torch.randint(1, 1000, (1,),
+                                                                                                    generator=g))
+    d = counts.cuda()
+    mask = E.count_pages(d).cpu()
+    want = (counts.view(nt, 256, 256) != 0).any(dim=2).to(torch.uint8)
+    assert torch.equal(mask, want)
+    lst = torch.nonzero(want.reshape(-1)).reshape(-1).to(torch.int32)
+    lst = lst[torch.randperm(lst.numel(), generator=g)].cuda()           # any order
+    comp = torch.empty((lst.numel(), 256), dtype=torch.int32, device="cuda")
+    E.counts_pack(d, lst, comp)
+    assert torch.equal(comp.cpu(), counts.view(-1, 256)[lst.cpu().long()])
+    out = torch.zeros_like(d)
+    E.counts_unpack(comp * 3, lst, out)
+    assert torch.equal(out.cpu(), counts * 3)
