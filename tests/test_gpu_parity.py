@@ -501,6 +501,23 @@ def test_autograd_function_matches_oracle():
     assert np.all(np.abs(dw - ref["dW"]) <= ulp16(ref["dW"], torch.bfloat16) + TOL * np.max(np.abs(ref["dW"])))
 
 
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 5e-3)])
+def test_dense_baseline_computes_the_oracle(dtype, tol):
+    """tools/dense_baseline.py (the dense |W|x|C| map of P:39 under torch autograd)
+    computes the oracle's W~, dW and dC_0 on CFG1: to 1e-9 with an fp64 map; with the fp32 map the
+    paper's PyTorch path would use, within 5e-3 (all-fp32 DKM loses ~1e-5..1e-3 here, DESIGN R7)."""
+    from tools.dense_baseline import dense_step
+    wl = synth.workload("cfg1")
+    W = synth.weights(wl, 0)
+    G = synth.grads(wl, 0)
+    C0 = synth.quantile_centroids(wl.k, wl.sigma)
+    Wt, dW, dC = dense_step(W.cuda(), G.cuda(), np.float32(C0).astype(np.float64), wl.tau, wl.max_iter, dtype)
+    ref = oracle_dense(bits_of(W), G.double().numpy(), C0, E.Params(wl.wdtype, wl.bits, wl.tau, wl.max_iter))
+    assert normwise(Wt.double().cpu().numpy(), ref["Wt"]) <= tol
+    assert normwise(dW.double().cpu().numpy(), ref["dW"]) <= tol
+    assert normwise(dC.double().cpu().numpy(), ref["dC"]) <= tol
+
+
 def test_launch_counts_are_native():
     W = synth.normal_tensor(10_000, 1.0, torch.bfloat16, 51).cuda()
     p = E.Params(torch.bfloat16, 3, 1e-3, 2)
