@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) f2_gather_kernel(const __grid_con
 // largest |G| of a 4K-element sample M to [2^21, 2^22).  An element with |G| >= 2^(24-s-f) goes
 // to the coarse bank as q = rint(G 2^s); a smaller one to the fine bank as q = rint(G 2^(s+f)).
 // Every |q| < 2^24.  For 16-bit G this is EXACT (no rounding at all) for every |G| in
-// [2^(7-s-f), 2^(24-s)) ~ [M 2^-(14+f), 4..8 M): a bf16 (fp16) value with |G| >= 2^e has its
+// [2^(7-s-f), 2^(24-s)) ~ [M 2^-(15+f), 4..8 M): a bf16 (fp16) value with |G| >= 2^e has its
 // last significand bit at 2^(e-7) (2^(e-10)), a multiple of 2^-s once e >= 7-s (10-s), which
 // f <= 17 (14) guarantees for every coarse element.  For fp32 G each element is split into both
 // banks: q_c = rint(G 2^s), and the exact residual G 2^s - q_c (|.| <= 1/2) as q_f = rint(. 2^f)
@@ -576,8 +576,10 @@ template <int GDT>
 struct B1Policy {
   static constexpr int kLoop = EDKM_B1_LOOP;
   static constexpr int GF32 = GDT == kFP32;
-  // fine-bank shift f (see above): bf16 <= 17, fp16 <= 14 keep every coarse element exact
-  static constexpr int kFine = GDT == kBF16 ? 16 : (GDT == kFP16 ? 14 : 24);
+  // fine-bank shift f (see above): bf16 <= 17, fp16 <= 14 keep every coarse element exact; at the
+  // bound, thrF = 2^(24-s-f) is exactly the smallest |G| the coarse bank holds exactly, so the
+  // fewest elements (and warps) need the fine bank
+  static constexpr int kFine = GDT == kBF16 ? 17 : (GDT == kFP16 ? 14 : 24);
   static constexpr uint32_t kSlots = 2 * kB1Pages * 256;  // slots per bank
   static constexpr uint32_t kFOff = kSlots * 4;           // byte offset of the fine bank
   static constexpr uint32_t kLoBias = 0x80000000u;
@@ -791,8 +793,11 @@ struct B1Policy {
     }
     const bool ok = GF32 ? gmax < glim : (max(gmax & 0xFFFFu, gmax >> 16) < glim16);
     if (active && max(rmax2 & 0xFFFFu, rmax2 >> 16) < win.np256 && ok) {
+      // the bank choice per element costs ~4 instructions per element, so it runs only for the warps
+      // that need it, and for the whole warp: a divergent warp would issue both paths (Gaussian fp16 G
+      // has a small element in ~1% of vectors, ~30% of warps: B1 4.37 -> 5.13 ms diverging, ncu r02)
       if (GF32) accumulate<2>(t, r, slot2);
-      else if (min(gmin2 & 0xFFFFu, gmin2 >> 16) >= thrm1) accumulate<0>(t, r, slot2);
+      else if (__all_sync(__activemask(), min(gmin2 & 0xFFFFu, gmin2 >> 16) >= thrm1)) accumulate<0>(t, r, slot2);
       else accumulate<1>(t, r, slot2);
     } else {
       // rare: re-read the 16 elements (dynamic indexing of the register vector would spill it)

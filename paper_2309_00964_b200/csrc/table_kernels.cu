@@ -574,6 +574,182 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   cluster.sync();
 }
 
+// ============================================================================ TB, split rows
+// The same reverse loop with each row's K centroids split over H adjacent lanes (KH = K/H each;
+// H = 1 in the build: see launch_tb_k) and the running psi kept in global memory (L2-resident:
+// 8 B per row) instead of shared memory.
+// TB<16> in one lane per row needs 128 registers (A, gh and the K accumulators in fp64) and
+// 100 KiB of staged rows: 16 warps per SM, and its per-row fp64 chains (s = sum_j A_j gh_j and
+// psi, 16 and 32 dependent adds) leave the FP64 pipe ~60% idle (ncu r01c).  Split over H = 2 lanes
+// every chain halves, a lane holds K/2 of the per-centroid state, and with v, n alone staged
+// (8 B per row) four CTAs fit per SM.  Sums over the row's centroids are combined by one xor
+// shuffle; the k-vector reduction over rows stays in fixed order (deterministic, rank-identical).
+template <int N, int NW, int H>
+__device__ __forceinline__ void cluster_allreduce_h(double (&v)[N / H], double* red, double* part, double* tot,
+                                                    int parity, cg::cluster_group& cluster) {
+  constexpr int NH = N / H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane % H;
+#pragma unroll
+  for (int n = 0; n < NH; ++n) {
+    double x = v[n];
+#pragma unroll
+    for (int o = 16; o >= H; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane < H) red[warp * N + sub * NH + n] = x;
+  }
+  __syncthreads();
+  double* mine = part + parity * N;
+  if (threadIdx.x < N) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w * N + threadIdx.x];
+    mine[threadIdx.x] = s;
+  }
+  cluster.sync();
+  if (threadIdx.x < N) {
+    double s = 0.0;
+    for (unsigned r = 0; r < cluster.num_blocks(); ++r) s += cluster.map_shared_rank(mine, r)[threadIdx.x];
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <int K, int H, int kStageB, int kMinBlocks>
+__global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_split_kernel(const TableArgs P) {
+  constexpr int KH = K / H;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double stage_mem[];
+  const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
+  const int sub = (tid & 31) % H, slot = tid / H, nslots = kBThreads / H;
+  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
+  __shared__ CSet<K> cs;
+  const double* sCt = cs.c;
+  const TensorState* st = P.state + t;
+  const int T = st->T, pcl = st->cl;
+  const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
+  const double* ctraj = P.ctraj + (int64_t)t * (P.max_iter + 1) * K;
+  const double* straj = P.straj + (int64_t)t * (P.max_iter > 0 ? P.max_iter : 1) * K;
+  double* psi_t = P.psi + (int64_t)t * kPatterns;
+  // this CTA owns partitions p = crank, crank + cl, ...; with pcl == cl (always, same heuristic
+  // in TF) that is the single partition `crank`, whose value and count are staged
+  const bool one = pcl == cl;
+  const int pb0 = one ? st->pbase[crank] : 0;
+  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem),
+             reinterpret_cast<int32_t*>(stage_mem) + kStageB, nullptr, nullptr, one ? st->nrows[crank] : 0,
+             P.wdtype, kStageB};
+  if (one) R.stage();
+  if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
+  __syncthreads();
+  const double h1 = 2.0 * P.inv_tau;
+  for (int it = T - 1; it >= 0; --it) {
+    cs.prepare(ctraj + (int64_t)it * K, P.inv_tau);
+    if (tid < K) {
+      const double cn = ctraj[(int64_t)(it + 1) * K + tid];
+      const double S = straj[(int64_t)it * K + tid];
+      const double is = S != 0.0 ? 1.0 / S : 0.0;
+      sInvS[tid] = is;
+      sG1[tid] = sG[tid] * is;
+      sG2[tid] = sG[tid] * cn * is;
+      sH2[tid] = h1 * ctraj[(int64_t)it * K + tid];
+    }
+    __syncthreads();
+    double acc[KH];
+#pragma unroll
+    for (int l = 0; l < KH; ++l) acc[l] = 0.0;
+    for (int p = crank; p < pcl; p += cl) {
+      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+      double* gpsi = psi_t + st->pbase[p];
+      const int nr = one ? R.nr : st->nrows[p];
+      // every lane of a row group runs the same trip count (the shuffles need the whole warp)
+      for (int r0 = slot - slot % (32 / H); r0 < nr; r0 += nslots) {
+        const int r = r0 + slot % (32 / H);
+        const bool live = r < nr && r0 < nr;
+        const int rr_ = live ? r : 0;
+        const double v = (nr > 0) ? (one ? R.v(rr_) : decode16(rows[rr_], P.wdtype)) : 0.0;
+        const double n = live ? (one ? R.n(rr_) : (double)cnt[rows[rr_]]) : 0.0;
+        double ps_old = 0.0;
+        if (live && sub == 0 && it != T - 1) ps_old = gpsi[r];  // issued early, used at the end
+        // attention of the row to this lane's KH centroids, normalised over all K (fp32, R7)
+        const float vf = (float)v;
+        const int jm = cs.nearest(vf);
+        const float v2 = 2.0f * vf;
+        float Af[KH];
+        float Z = 0.0f;
+#pragma unroll
+        for (int jj = 0; jj < KH; ++jj) {
+          const int j = sub * KH + jj;
+          Af[jj] = ex2(fmaf(-cs.dms[jm][j], v2 - cs.ph[jm][j], cs.dpl[jm][j]));
+          Z += Af[jj];
+        }
+        if (H == 2) Z += __shfl_xor_sync(0xffffffffu, Z, 1);
+        const float iz = 1.0f / Z;
+        double A[KH], gh[KH];
+        double s = 0.0, dpsi = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < KH; ++jj) {
+          const int j = sub * KH + jj;
+          A[jj] = (double)(Af[jj] * iz);
+          gh[jj] = fma(sG1[j], v, -sG2[j]);  // dL/dA_t[u][j] (zero where S_t[j] = 0)
+          s = fma(A[jj], gh[jj], s);
+          dpsi = fma(A[jj], sG1[j], dpsi);   // direct path of v through M_t
+        }
+        if (H == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
+#pragma unroll
+        for (int jj = 0; jj < KH; ++jj) {
+          const int l = sub * KH + jj;
+          const double rr = A[jj] * (gh[jj] - s);     // softmax Jacobian applied to gh
+          const double q = rr * fma(h1, v, -sH2[l]);  // rr * dz_l, dz_l = 2 (v - C_t[l]) / tau
+          dpsi -= q;
+          acc[jj] = fma(n, q, acc[jj]);
+        }
+        if (H == 2) dpsi += __shfl_xor_sync(0xffffffffu, dpsi, 1);
+        if (live && sub == 0) gpsi[r] = ps_old + dpsi;
+      }
+    }
+    cluster_allreduce_h<K, kBThreads / 32, H>(acc, red, part, tot, it & 1, cluster);
+    if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
+    __syncthreads();
+  }
+  if (crank == 0 && tid < K) P.dC0[(int64_t)t * K + tid] = (float)sG[tid];
+  // (phi, psi) table: phi[u] = (2/tau) sum_l A_T[u,l] (C_T[l] - W~_u)^2 (one row per thread)
+  cs.prepare(ctraj + (int64_t)T * K, P.inv_tau);
+  __syncthreads();
+  float2* pp = P.phipsi + (int64_t)t * kPatterns;
+  for (int p = crank; p < pcl; p += cl) {
+    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
+    const double* gpsi = psi_t + st->pbase[p];
+    const int nr = one ? R.nr : st->nrows[p];
+    for (int r = tid; r < nr; r += kBThreads) {
+      const uint32_t u = rows[r];
+      const double v = one ? R.v(r) : decode16(u, P.wdtype);
+      float Af[K];
+      attention_row<K>((float)v, cs, Af);
+      double wt = 0.0;
+#pragma unroll
+      for (int l = 0; l < K; ++l) wt = fma((double)Af[l], sCt[l], wt);
+      double var = 0.0;
+#pragma unroll
+      for (int l = 0; l < K; ++l) var += (double)Af[l] * (sCt[l] - wt) * (sCt[l] - wt);
+      pp[u] = make_float2((float)(2.0 * P.inv_tau * var), T > 0 ? (float)gpsi[r] : 0.0f);
+    }
+    const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+    for (int u0 = st->pbase[p] + tid * 16; u0 < st->pbase[p + 1]; u0 += kBThreads * 16) {
+      const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
+      int c[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 x = __ldg(c4 + q);
+        c[4 * q] = x.x;
+        c[4 * q + 1] = x.y;
+        c[4 * q + 2] = x.z;
+        c[4 * q + 3] = x.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (!pattern_finite(u0 + e, P.wdtype) || c[e] == 0) pp[u0 + e] = nan2;
+    }
+  }
+  cluster.sync();
+}
+
 // ============================================================================ launchers
 // CTAs per tensor (row partitions, <= the portable cluster size 8): fill the GPU for small nt,
 // else 2 for bf16 and 4 for fp16.  Rows are balanced across the partitions, but each CTA pays
@@ -638,8 +814,24 @@ cudaError_t launch_tf(const TableArgs& P, cudaStream_t s) {
   }
 }
 EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
+// TB variant per k (measured, S4): k <= 8 run tb_split_kernel with one lane per row and
+// psi in global memory, four CTAs per SM (CFG3 k = 8 TB 0.241 -> 0.217 ms, CFG4 k = 4 1.79 ->
+// 1.43 ms); k = 16 keeps tb_kernel (128 registers, psi staged): split over two lanes it measured
+// 3.67 -> 5.2-5.6 ms (duplicated nearest-centroid search, runtime centroid offsets, shuffles).
+#ifndef EDKM_TB_SPLIT_MAXK
+#define EDKM_TB_SPLIT_MAXK 8
+#endif
+#ifndef EDKM_TB_H2_MINK
+#define EDKM_TB_H2_MINK 32
+#endif
 template <int K>
 static cudaError_t launch_tb_k(const TableArgs& P, cudaStream_t s) {
+  if (K <= EDKM_TB_SPLIT_MAXK) {
+    constexpr int H = K >= EDKM_TB_H2_MINK ? 2 : 1, MB = 4;
+    if (P.wdtype == kBF16)
+      return launch_table(P, s, tb_split_kernel<K, H, kStageB16, MB>, (size_t)kStageB16 * 8, kBThreads);
+    return launch_table(P, s, tb_split_kernel<K, H, kStageB32, MB>, (size_t)kStageB32 * 8, kBThreads);
+  }
   if (P.wdtype == kBF16)
     return launch_table(P, s, tb_kernel<K, kBThreads, kStageB16>, (size_t)kStageB16 * 16, kBThreads);
   return launch_table(P, s, tb_kernel<K, kBThreads, kStageB32>, (size_t)kStageB32 * 16, kBThreads);
