@@ -117,9 +117,12 @@ edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_
  * reached nranks x epoch (acquire).  After it, the local view of the buffer holds the global
  * counts on every rank -- exact (integer).  No host synchronisation.  Requires NVLS multicast
  * support; callers without it use edkm_uniquify + an all-reduce.
- *   emulate   : 1 = the same protocol on ordinary device memory with plain atomics (nranks
- *               must be 1; `*_mc` are then the buffers themselves) -- for testing the
- *               protocol on a system without multicast.  0 otherwise. */
+ *   emulate   : 1 = the same protocol on ordinary device memory with plain atomics -- for
+ *               testing it on a system without multicast; `*_mc` are then this rank's own
+ *               buffers.  nranks 1, or 2 with peer_delta: every add (and arrival) goes to this
+ *               rank's copy and to the peer's copy at byte offset peer_delta (the peer's buffer
+ *               mapped into this process by edkm_ipc_open), as the switch adds into every
+ *               rank's copy -- a real second writer.  0 otherwise (peer_delta ignored). */
 #define EDKM_NVLS_FLAGS 1024
 typedef struct {
     int32_t* counts_mc;
@@ -128,6 +131,7 @@ typedef struct {
     uint32_t* epoch;
     int nranks;
     int emulate;
+    int64_t peer_delta;
 } edkm_nvls;
 edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* nvls, void* stream);
 
@@ -164,6 +168,16 @@ edkm_status edkm_mc_add_device(edkm_mcbuf* buf);
 edkm_status edkm_mc_bind(edkm_mcbuf* buf, void** local_out, void** mc_out);
 edkm_status edkm_mc_destroy(edkm_mcbuf* buf);
 const char* edkm_mc_last_error(void);
+
+/* CUDA IPC of a device buffer between processes (the emulate mode's second writer, above):
+ * edkm_ipc_handle writes the 64-byte handle of dev_ptr's allocation to host memory handle_out and
+ * dev_ptr's byte offset in that allocation to *offset_out; edkm_ipc_open maps another process's
+ * handle into this one (*dev_ptr_out = the allocation's base: add the owner's offset);
+ * edkm_ipc_close unmaps it.  EDKM_E_ARG for NULL pointers, EDKM_E_CUDA (edkm_mc_last_error) on
+ * failure. */
+edkm_status edkm_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out);
+edkm_status edkm_ipc_open(const void* handle, void** dev_ptr_out);
+edkm_status edkm_ipc_close(void* dev_ptr);
 
 /* TF -- forward table phase (DKM iterations on the attention table).
  *   counts : [nt][65536] int32, global over ranks.

@@ -210,6 +210,7 @@ size_t edkm_workspace_bytes(int nt, const edkm_params* p) {
 
 edkm_status edkm_uniquify(const edkm_tensor* tensors, int nt, int wdtype, int32_t* counts, edkm_comm* comm,
                           void* stream) {
+  EDKM_NVTX("edkm F1 uniquify");
   g_launches = 0;
   if (wdtype != EDKM_BF16 && wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");
   edkm_status st = check_tensors(tensors, nt);
@@ -241,13 +242,15 @@ edkm_status edkm_nvls_failed(int* failed) {
 }
 
 edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, const edkm_nvls* x, void* stream) {
+  EDKM_NVTX("edkm F1 uniquify (NVLS)");
   g_launches = 0;
   if (wdtype != EDKM_BF16 && wdtype != EDKM_FP16) return fail(EDKM_E_DTYPE, "wdtype must be BF16 or FP16");
   edkm_status st = check_tensors(tensors, nt);
   if (st != EDKM_OK) return st;
   if (!x || !x->counts_mc || !x->flags_mc || !x->flags || !x->epoch) return fail(EDKM_E_ARG, "NULL NVLS buffer");
   if (x->nranks < 1) return fail(EDKM_E_ARG, "nranks < 1");
-  if (x->emulate && x->nranks != 1) return fail(EDKM_E_ARG, "emulate requires nranks == 1");
+  if (x->emulate && !(x->nranks == 1 || (x->nranks == 2 && x->peer_delta != 0)))
+    return fail(EDKM_E_ARG, "emulate requires nranks == 1, or nranks == 2 with a peer buffer");
   if (nt > kMaxTensorsPerLaunch) return fail(EDKM_E_UNSUPPORTED, "NVLS uniquify takes at most 512 tensors per call");
   const int sms = sm_count();
   if (sms > EDKM_NVLS_FLAGS) return fail(EDKM_E_UNSUPPORTED, "more SMs than NVLS arrival counters");
@@ -263,6 +266,7 @@ edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, c
     A.offs[i + 1] = A.offs[i] + tensors[i].n;
   }
   A.total = A.offs[nt];
+  A.peer_delta = x->emulate ? x->peer_delta : 0;
   cudaError_t e = launch_f1_nvls(A, x->counts_mc, x->flags_mc, x->flags, x->epoch, x->nranks, x->emulate, sms,
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "F1 NVLS histogram launch");
@@ -272,6 +276,7 @@ edkm_status edkm_uniquify_nvls(const edkm_tensor* tensors, int nt, int wdtype, c
 
 edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p, const float* C0,
                                float* C_out, float* table, void* saved, void* stream) {
+  EDKM_NVTX("edkm TF forward");
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
@@ -303,6 +308,7 @@ edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, co
 edkm_status edkm_reconstruct(const edkm_tensor* tensors, int nt, const edkm_params* p, const float* table,
                              const float* C_out, const void* saved, int mode, int out_dtype, void* const* out,
                              void* stream) {
+  EDKM_NVTX("edkm F2 reconstruct");
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
@@ -354,6 +360,7 @@ static edkm_status check_backward(const edkm_tensor* tensors, int nt, const edkm
 
 edkm_status edkm_backward_buckets(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
                                   int gdtype, const void* saved, void* ws, void* stream) {
+  EDKM_NVTX("edkm B1 buckets");
   g_launches = 0;
   edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
   if (st != EDKM_OK) return st;
@@ -378,6 +385,7 @@ edkm_status edkm_backward_buckets(const edkm_tensor* tensors, int nt, const edkm
 
 edkm_status edkm_backward_gamma(int nt, const edkm_params* p, const int32_t* counts, const void* saved, void* ws,
                                 double* gamma, void* stream) {
+  EDKM_NVTX("edkm TGAMMA");
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
@@ -413,6 +421,7 @@ edkm_status edkm_backward_reduce(const edkm_tensor* tensors, int nt, const edkm_
 
 edkm_status edkm_backward_table_range(int nt, int t0, int t1, const edkm_params* p, const int32_t* counts,
                                       const void* saved, void* ws, const double* gamma, float* dC0, void* stream) {
+  EDKM_NVTX("edkm TB table backward");
   g_launches = 0;
   edkm_status st = check_params(p);
   if (st != EDKM_OK) return st;
@@ -464,6 +473,7 @@ edkm_status edkm_layout(int nt, const edkm_params* p, size_t* saved_offs, size_t
 edkm_status edkm_backward_dw(const edkm_tensor* tensors, int nt, const edkm_params* p, const void* const* grads,
                              int gdtype, const void* saved, const void* ws, void* const* dW, int dw_dtype,
                              void* stream) {
+  EDKM_NVTX("edkm B2 dW");
   g_launches = 0;
   edkm_status st = check_backward(tensors, nt, p, grads, gdtype);
   if (st != EDKM_OK) return st;

@@ -81,6 +81,7 @@ struct StreamArgs {
   int gdtype;                 // gradient dtype (kBF16/kFP16/kFP32) for B1/B2
   int odtype;                 // output dtype for F2/B2
   int mode;                   // F2 mode
+  int64_t peer_delta;         // F1, NVLS emulate with a peer: byte offset of the peer's copy (0: none)
   int64_t total;              // sum of n
   int64_t offs[kMaxTensorsPerLaunch + 1];
   const uint16_t* w[kMaxTensorsPerLaunch];

@@ -132,6 +132,7 @@ namespace edkm {
 // F1's all-reduce of the counts, and B1's all-reduce of gamma_T, on the caller's stream (api.cu)
 edkm_status comm_allreduce_sum(edkm_comm* comm, void* buf, size_t count, int fp64, cudaStream_t s) {
   if (!comm || count == 0) return EDKM_OK;
+  EDKM_NVTX(fp64 ? "edkm allreduce gamma" : "edkm allreduce counts");
   const ncclResult_t r = nccl().AllReduce(buf, buf, count, fp64 ? ncclFloat64 : ncclInt32, ncclSum, comm->c, s);
   return r == ncclSuccess ? EDKM_OK : nccl_fail(r, fp64 ? "ncclAllReduce(gamma)" : "ncclAllReduce(counts)");
 }
@@ -199,6 +200,7 @@ edkm_status edkm_comm_allreduce(edkm_comm* comm, void* buf, size_t count, int dt
   }
   if (op != EDKM_SUM && op != EDKM_MAX) return set_error(EDKM_E_ARG, "op must be EDKM_SUM or EDKM_MAX");
   if (count == 0) return EDKM_OK;
+  EDKM_NVTX("edkm comm allreduce");
   const ncclResult_t r = nccl().AllReduce(buf, buf, count, t, op == EDKM_SUM ? ncclSum : ncclMax, comm->c,
                                           (cudaStream_t)stream);
   return r == ncclSuccess ? EDKM_OK : nccl_fail(r, "ncclAllReduce");
@@ -208,6 +210,7 @@ edkm_status edkm_comm_allgather(edkm_comm* comm, const void* send, void* recv, s
   if (!comm) return set_error(EDKM_E_ARG, "comm is NULL");
   if (bytes_per_rank > 0 && (!send || !recv)) return set_error(EDKM_E_ARG, "send or recv is NULL");
   if (bytes_per_rank == 0) return EDKM_OK;
+  EDKM_NVTX("edkm comm allgather");
   cudaStream_t s = (cudaStream_t)stream;
   const ncclResult_t r = nccl().AllGather(send, recv, bytes_per_rank, ncclUint8, comm->c, s);
   return r == ncclSuccess ? EDKM_OK : nccl_fail(r, "ncclAllGather");

@@ -1,6 +1,7 @@
 // launch.h -- internal launcher declarations shared by the .cu files of libedkm.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "../../include/edkm.h"
@@ -14,6 +15,14 @@ namespace edkm {
 edkm_status set_error(edkm_status st, const char* msg);
 void reset_launches();
 void add_launches(int n);
+// NVTX range around an entry point's launches (SURVEY S5 tracing): nsys / ncu --nvtx show each
+// kernel and collective of the step under its phase name.  Header-only NVTX v3: a no-op unless a
+// tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define EDKM_NVTX(name) ::edkm::NvtxRange edkm_nvtx_range_(name)
 // in-place sum all-reduce over the library's NCCL communicator (exchange.cu); comm == NULL: no-op
 edkm_status comm_allreduce_sum(edkm_comm* comm, void* buf, size_t count, int fp64, cudaStream_t s);
 

@@ -42,7 +42,9 @@ typedef CUresult (*PFN_cuMemImportFromShareableHandle_v12000)(CUmemGenericAlloca
 typedef CUresult (*PFN_cuMemGetAllocationGranularity_v12000)(size_t*, const CUmemAllocationProp*,
                                                             CUmemAllocationGranularity_flags);
 typedef CUresult (*PFN_cuDeviceGetAttribute_v12000)(int*, CUdevice_attribute, CUdevice);
+typedef CUresult (*PFN_cuMemGetAddressRange_v12000)(CUdeviceptr*, size_t*, CUdeviceptr);
 EDKM_DRV(cuDeviceGetAttribute)
+EDKM_DRV(cuMemGetAddressRange)
 EDKM_DRV(cuMulticastCreate)
 EDKM_DRV(cuMulticastAddDevice)
 EDKM_DRV(cuMulticastBindMem)
@@ -70,7 +72,7 @@ bool resolve() {
     if (cudaGetDriverEntryPoint(#name, &f, cudaEnableDefault, &q) != cudaSuccess || !f) ok = false; \
     p_##name = reinterpret_cast<decltype(p_##name)>(f);                                          \
   }
-  R(cuDeviceGetAttribute) R(cuMulticastCreate) R(cuMulticastAddDevice) R(cuMulticastBindMem) R(cuMulticastUnbind)
+  R(cuDeviceGetAttribute) R(cuMemGetAddressRange) R(cuMulticastCreate) R(cuMulticastAddDevice) R(cuMulticastBindMem) R(cuMulticastUnbind)
   R(cuMulticastGetGranularity) R(cuMemCreate) R(cuMemRelease) R(cuMemAddressReserve) R(cuMemAddressFree)
   R(cuMemMap) R(cuMemUnmap) R(cuMemSetAccess) R(cuMemExportToShareableHandle) R(cuMemImportFromShareableHandle)
   R(cuMemGetAllocationGranularity)
@@ -187,6 +189,48 @@ edkm_status edkm_mc_bind(edkm_mcbuf* b, void** local_out, void** mc_out) {
   *local_out = (void*)b->uva;
   *mc_out = (void*)b->mva;
   return EDKM_OK;
+}
+
+// CUDA IPC plumbing of the NVLS protocol's emulation with a real second writer (edkm_nvls.peer_delta):
+// another process's device buffer mapped into this one (runtime API; no compute).
+edkm_status edkm_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return EDKM_E_ARG;
+  // the handle maps the whole allocation: dev_ptr's offset in it (a caching allocator sub-allocates)
+  if (!resolve()) {
+    snprintf(g_nvls_err, sizeof(g_nvls_err), "CUDA driver entry points unavailable");
+    return EDKM_E_CUDA;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  const CUresult r = p_cuMemGetAddressRange(&base, &size, (CUdeviceptr)dev_ptr);
+  if (r != CUDA_SUCCESS) return drv_fail(r, "cuMemGetAddressRange");
+  *offset_out = (size_t)((CUdeviceptr)dev_ptr - base);
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) {
+    snprintf(g_nvls_err, sizeof(g_nvls_err), "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    return EDKM_E_CUDA;
+  }
+  memcpy(handle_out, &h, sizeof(h));
+  return EDKM_OK;
+}
+
+edkm_status edkm_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return EDKM_E_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    snprintf(g_nvls_err, sizeof(g_nvls_err), "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return EDKM_E_CUDA;
+  }
+  return EDKM_OK;
+}
+
+edkm_status edkm_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return EDKM_OK;
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? EDKM_OK : EDKM_E_CUDA;
 }
 
 edkm_status edkm_mc_destroy(edkm_mcbuf* b) {

@@ -92,11 +92,17 @@ __device__ __forceinline__ uint32_t pat(const V8& v, int e) { return (v.x[e >> 1
 // Adds to the global counts: a plain L2 atomic, or (MC, NVLS mode) a multimem reduction on the
 // multicast address of a symmetric buffer -- the NVSwitch adds v into every rank's copy, so the
 // cross-rank sum of the counts happens inside F1's own flushes, with no separate collective.
-// MC = 0: plain; 1: NVLS multicast; 2: the same protocol on ordinary memory (one rank: tests).
+// MC = 0: plain; 1: NVLS multicast; 2: the same protocol on ordinary memory (tests): the add goes
+// to this rank's copy and, with a peer (peer != 0: byte offset of the peer's copy mapped by CUDA
+// IPC), to the peer's copy too -- what the switch does for every rank's copy.
 template <int MC>
-__device__ __forceinline__ void cnt_add(int32_t* p, int v) {
-  if (MC == 1) asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-  else atomicAdd(p, v);
+__device__ __forceinline__ void cnt_add(int32_t* p, int v, int64_t peer = 0) {
+  if (MC == 1) {
+    asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    atomicAdd(p, v);
+    if (MC == 2 && peer) atomicAdd_system(reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p) + peer), v);
+  }
 }
 
 template <int MC>
@@ -116,7 +122,7 @@ struct F1Policy {
   __device__ void load(int t, int64_t i, Vec& r) const { r.w = ldg_stream8(A.w[t] + i); }
   __device__ void count(int t, uint32_t u) {
     if (u < (uint32_t)kF1Bins) red_shared_add(&h[u], 1u);
-    else cnt_add<MC>(&cnt(t)[u], 1);
+    else cnt_add<MC>(&cnt(t)[u], 1, A.peer_delta);
   }
   __device__ void process(int t, int64_t, const Vec& r) {
 #pragma unroll
@@ -128,7 +134,7 @@ struct F1Policy {
     int32_t* c = cnt(t);
     for (int i = threadIdx.x; i < kF1Bins; i += blockDim.x) {
       const uint32_t v = h[i];
-      if (v) cnt_add<MC>(&c[i], (int32_t)v);
+      if (v) cnt_add<MC>(&c[i], (int32_t)v, A.peer_delta);
     }
     __syncthreads();
   }
@@ -166,7 +172,7 @@ constexpr size_t kF1Smem = (size_t)(kF1LRows + 1) * 128 > (size_t)kF1Bins * 4
                                ? (size_t)(kF1LRows + 1) * 128 : (size_t)kF1Bins * 4;
 
 template <int MC>
-__device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u) { cnt_add<MC>(&c[u], 1); }
+__device__ __forceinline__ void f1_count_global(int32_t* c, uint32_t u, int64_t peer) { cnt_add<MC>(&c[u], 1, peer); }
 
 // fold the 32 copies of rows tid and tid+1024 into acc (pos, neg per row) and zero them
 __device__ __forceinline__ void f1l_fold(uint32_t* h, uint32_t acc[4]) {
@@ -241,8 +247,15 @@ __global__ void __launch_bounds__(kThreads, 1) f1_hist_kernel(const __grid_const
   if (MC) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (MC == 1) asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
-      else asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+      if (MC == 1) {
+        asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+      } else {
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+        if (A.peer_delta)
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(reinterpret_cast<char*>(flags_mc + blockIdx.x) +
+                                                                        A.peer_delta)
+                       : "memory");
+      }
     }
   }
 }
@@ -322,8 +335,8 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
       const int64_t head = min((int64_t)(((32u - (uint32_t)(wa & 31u)) & 31u) >> 1), b - a);
       const int64_t va = a + head;
       const int64_t nv = (b - va) >> 4;
-      for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global<MC>(cnt, w[i]);
-      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global<MC>(cnt, w[i]);
+      for (int64_t i = a + tid; i < a + head; i += bs) f1_count_global<MC>(cnt, w[i], A.peer_delta);
+      for (int64_t i = va + 16 * nv + tid; i < b; i += bs) f1_count_global<MC>(cnt, w[i], A.peer_delta);
       // one 16-pattern vector.  Every lane takes the same straight-line path: a pattern outside
       // the window is clamped to the trash row kF1LRows (never folded), and the lanes holding
       // such a pattern (~0.1% of bf16 N(0, 0.02^2) weights, but ~40% of warp iterations see one)
@@ -356,8 +369,8 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
           for (int q = 0; q < 8; ++q) {
             const uint32_t x = r.x[q];
             const uint32_t rel = __vadd2(x & 0x7FFF7FFFu, pb2);
-            if ((rel & 0xFFFFu) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x & 0xFFFFu);
-            if ((rel >> 16) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x >> 16);
+            if ((rel & 0xFFFFu) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x & 0xFFFFu, A.peer_delta);
+            if ((rel >> 16) >= (uint32_t)kF1LRows) f1_count_global<MC>(cnt, x >> 16, A.peer_delta);
           }
         }
       };
@@ -382,8 +395,8 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
         const int r = tid + j * 1024;
         if (r < kF1LRows) {
           const uint32_t u = ((uint32_t)s_base << 8) + (uint32_t)r;
-          if (acc[2 * j]) cnt_add<MC>(&cnt[u], (int32_t)acc[2 * j]);
-          if (acc[2 * j + 1]) cnt_add<MC>(&cnt[u | 0x8000u], (int32_t)acc[2 * j + 1]);
+          if (acc[2 * j]) cnt_add<MC>(&cnt[u], (int32_t)acc[2 * j], A.peer_delta);
+          if (acc[2 * j + 1]) cnt_add<MC>(&cnt[u | 0x8000u], (int32_t)acc[2 * j + 1], A.peer_delta);
         }
       }
       __syncthreads();

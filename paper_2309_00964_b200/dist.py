@@ -235,9 +235,10 @@ class NvlsCounts:
     this step's F1, so no rank can add into a copy another rank has not cleared -- and
     NVLS_FLAGS monotonic arrival counters; plus this rank's epoch.  Rank 0 creates the object
     and passes its file descriptor to the other ranks over a local socket (SCM_RIGHTS).
-    Raises NvlsUnavailable when the system has no NVLS multicast.  emulate=True (one rank
-    only) runs the same protocol -- kernels, epochs, alternating buffers -- on ordinary
-    device memory with plain atomics, to test it where multicast objects cannot be created.
+    Raises NvlsUnavailable when the system has no NVLS multicast.  emulate=True runs the same
+    protocol -- kernels, epochs, alternating buffers -- on ordinary device memory with plain
+    atomics, to test it where multicast objects cannot be created: one rank, or two ranks (e.g.
+    two processes on one GPU) whose F1 adds into both ranks' copies through CUDA IPC.
     """
 
     def __init__(self, nt: int, device, group=None, emulate: bool = False):
@@ -256,14 +257,36 @@ class NvlsCounts:
         self._nt = nt
         self.step_index = 0
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.peer_delta = 0
         if self.emulate:
-            if self.nranks != 1:
-                raise ValueError("emulate requires a single rank")
+            # the protocol on ordinary memory: one rank, or two ranks each adding into both copies
+            # (its own and the peer's, mapped by CUDA IPC) as the switch would -- a real second writer
+            if self.nranks > 2:
+                raise ValueError("emulate supports one or two ranks")
             self._buf = None
-            self.bufs = [torch.zeros((max(nt, 1), 65536), dtype=torch.int32, device=dev) for _ in range(2)]
-            self.flags = torch.zeros(NVLS_FLAGS, dtype=torch.int32, device=dev)
+            cb = (max(nt, 1) * 65536 * 4 + 255) // 256 * 256
+            self._emu = torch.zeros(2 * cb + NVLS_FLAGS * 4, dtype=torch.uint8, device=dev)
+            self.bufs = [self._emu[o:o + cb].view(torch.int32)[:max(nt, 1) * 65536].view(max(nt, 1), 65536)
+                         for o in (0, cb)]
+            self.flags = self._emu[2 * cb:].view(torch.int32)
             self.mc_ptrs = [t.data_ptr() for t in self.bufs] + [self.flags.data_ptr()]
             self.current = self.bufs[0][:nt]
+            self._peer = None
+            if self.nranks == 2:
+                h, off = (ctypes.c_uint8 * 64)(), ctypes.c_size_t(0)
+                if L.edkm_ipc_handle(ctypes.c_void_p(self._emu.data_ptr()), h, ctypes.byref(off)) != 0:
+                    raise NvlsUnavailable(f"edkm_ipc_handle: {L.edkm_mc_last_error().decode()}")
+                objs = [None, None]
+                dist.all_gather_object(objs, (bytes(h), off.value), group=group)
+                ph, poff = objs[1 - rank]
+                base = ctypes.c_void_p()
+                hb = (ctypes.c_uint8 * 64).from_buffer_copy(ph)
+                if L.edkm_ipc_open(hb, ctypes.byref(base)) != 0:
+                    raise NvlsUnavailable(f"edkm_ipc_open: {L.edkm_mc_last_error().decode()}")
+                self._peer = base
+                self.peer_delta = base.value + poff - self._emu.data_ptr()
+                torch.cuda.synchronize(dev)
+                dist.barrier(group)
             return
         self._dev = dev
         sup = ctypes.c_int(0)
@@ -350,10 +373,16 @@ class NvlsCounts:
             self.bufs[nxt].zero_()
         self.current = self.bufs[cur][:self._nt]
         return E._Nvls(self.mc_ptrs[cur], self.mc_ptrs[2], self.flags.data_ptr(), self.epoch.data_ptr(), self.nranks,
-                       int(self.emulate))
+                       int(self.emulate), self.peer_delta)
 
     def close(self):
         from . import edkm as E
+        if getattr(self, "_peer", None) is not None:
+            torch.cuda.synchronize()
+            if self.nranks > 1:
+                dist.barrier(self.group)  # the peer's last adds into our copy are done
+            E.lib().edkm_ipc_close(self._peer)
+            self._peer = None
         if getattr(self, "_buf", None) is not None and self._buf.value:
             torch.cuda.synchronize()
             self.bufs = self.flags = self.current = None

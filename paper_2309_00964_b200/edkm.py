@@ -46,7 +46,8 @@ class _Tensor(ctypes.Structure):
 
 class _Nvls(ctypes.Structure):
     _fields_ = [("counts_mc", ctypes.c_void_p), ("flags_mc", ctypes.c_void_p), ("flags", ctypes.c_void_p),
-                ("epoch", ctypes.c_void_p), ("nranks", ctypes.c_int), ("emulate", ctypes.c_int)]
+                ("epoch", ctypes.c_void_p), ("nranks", ctypes.c_int), ("emulate", ctypes.c_int),
+                ("peer_delta", ctypes.c_int64)]
 
 
 NVLS_FLAGS = 1024
@@ -99,6 +100,9 @@ def lib():
             "edkm_mc_bind": ([P, P, P], i32),
             "edkm_mc_destroy": ([P], i32),
             "edkm_mc_last_error": ([], ctypes.c_char_p),
+            "edkm_ipc_handle": ([P, P, P], i32),
+            "edkm_ipc_open": ([P, P], i32),
+            "edkm_ipc_close": ([P], i32),
             "edkm_set_max_ctas": ([i32], i32),
             "edkm_comm_unique_id": ([P], i32),
             "edkm_comm_init": ([P, P, i32, i32], i32),
@@ -129,7 +133,7 @@ def exported_symbols() -> list:
             "edkm_mc_supported", "edkm_mc_create", "edkm_mc_import", "edkm_mc_bytes", "edkm_mc_add_device",
             "edkm_mc_bind", "edkm_mc_destroy", "edkm_mc_last_error", "edkm_comm_unique_id", "edkm_comm_init",
             "edkm_comm_destroy", "edkm_comm_info", "edkm_comm_allreduce", "edkm_comm_allgather", "edkm_count_pages",
-            "edkm_counts_pack", "edkm_counts_unpack"]
+            "edkm_counts_pack", "edkm_counts_unpack", "edkm_ipc_handle", "edkm_ipc_open", "edkm_ipc_close"]
 
 
 def _check(rc: int, what: str):

@@ -142,10 +142,9 @@ def _nvls_worker(port, q, emulate):
                   for i, n in enumerate(SIZES)]
             if step == 3:  # an fp16-like spread: the shared-array path of F1
                 Ws[0] = torch.randint(0, 65536, (SIZES[0],), dtype=torch.int32).to(torch.int16).view(torch.bfloat16).to(dev)
-            got = plan.uniquify_nvls(Ws, nv).clone()
-            want = ref.uniquify(Ws).clone()
-            torch.cuda.synchronize()
-            res.append(bool(torch.equal(got, want)))
+            got = plan.uniquify_nvls(Ws, nv).cpu().numpy()
+            want = np.stack([O.histogram(w.view(torch.int16).cpu().numpy().view(np.uint16)) for w in Ws])
+            res.append(bool(np.array_equal(got, want.astype(np.int32))))  # against the oracle
         Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 800 + i).to(dev) for i, n in enumerate(SIZES)]
         Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 900 + i).to(dev) for i, n in enumerate(SIZES)]
         C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
@@ -277,3 +276,88 @@ def test_page_exchange_kernels(nt):
     out = torch.zeros_like(d)
     E.counts_unpack(comp * 3, lst, out)
     assert torch.equal(out.cpu(), counts * 3)
+
+
+def _nvls2_worker(rank, world, port, q):
+    """Two processes on the one B200, each F1-ing its slices with the NVLS protocol in emulate mode:
+    every add and arrival goes into both ranks' count copies (the peer's mapped by CUDA IPC), so the
+    arrival barrier, epochs and alternating buffers run with a real second writer."""
+    from paper_2309_00964_b200.dist import NvlsCounts
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    try:
+        p = E.Params(torch.bfloat16, **P_)
+        nv = NvlsCounts(len(SIZES), dev, emulate=True)
+        plan = E.Plan([b - a for a, b in shard_all(SIZES, rank, world)], p, dev)
+        got = []
+        for step in range(5):
+            Ws = [synth.normal_tensor(n, 1.0 + step, torch.bfloat16, 700 + 10 * step + i) for i, n in enumerate(SIZES)]
+            if step == 3:  # uniformly random bits: the shared-array path of F1 and the global atomics
+                Ws[0] = synth.random_bits(SIZES[0], 55).view(torch.bfloat16)
+            Wl = [w[a:b].contiguous().to(dev) for w, (a, b) in zip(Ws, shard_all(SIZES, rank, world))]
+            got.append(plan.uniquify_nvls(Wl, nv).cpu().numpy().copy())
+        # one full sharded step with the fused exchange (gamma through gloo)
+        Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
+        Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i) for i, n in enumerate(SIZES)]
+        rng = shard_all(SIZES, rank, world)
+        Wl = [w[a:b].contiguous().to(dev) for w, (a, b) in zip(Ws, rng)]
+        Gl = [g[a:b].contiguous().to(dev) for g, (a, b) in zip(Gs, rng)]
+        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(SIZES), dtype=torch.float32, device=dev)
+        outs = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
+        dW = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
+        ShardedStep(plan, allreduce=_reduce_via_host, nvls=nv)(Wl, Gl, C0, outs, dW)
+        torch.cuda.synchronize()
+        q.put((rank, got, int(nv.epoch.item()), plan.C_out.cpu().numpy(), plan.dC0.cpu().numpy(),
+               [o.cpu().double().numpy() for o in outs], [d.cpu().double().numpy() for d in dW]))
+        nv.close()
+    except Exception as e:
+        q.put((rank, "err", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nvls_protocol_two_writers_matches_oracle():
+    """the fused count exchange against O.histogram (not CUDA F1), with two writers."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_nvls2_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=600)
+        res[r[0]] = r
+    for pr in procs:
+        pr.join(timeout=120)
+    for r in range(world):
+        assert res[r][1] != "err", res[r]
+    for step in range(5):
+        Ws = [synth.normal_tensor(n, 1.0 + step, torch.bfloat16, 700 + 10 * step + i) for i, n in enumerate(SIZES)]
+        if step == 3:
+            Ws[0] = synth.random_bits(SIZES[0], 55).view(torch.bfloat16)
+        for t, w in enumerate(Ws):
+            ref = O.histogram(w.view(torch.int16).numpy().view(np.uint16)).astype(np.int32)
+            for r in range(world):
+                assert np.array_equal(res[r][1][step][t], ref), (step, t, r)
+    for r in range(world):
+        assert res[r][2] == 6  # five uniquify_nvls steps + the ShardedStep's
+    k = 1 << P_["bits"]
+    C0 = np.float32(synth.quantile_centroids(k, 1.0)).astype(np.float64)
+    for t, n in enumerate(SIZES):
+        W = synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + t)
+        G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + t)
+        w = O.decode16(W.view(torch.int16).numpy().view(np.uint16), O.BF16)
+        Ct, St, _ = O.dkm_forward(w, C0, P_["tau"], P_["max_iter"])
+        Wt = O.reconstruct(w, Ct[-1], P_["tau"])
+        dWr, dC = O.dkm_backward(w, G.double().numpy(), Ct, St, P_["tau"])
+        assert np.array_equal(res[0][3][t], res[1][3][t]) and np.array_equal(res[0][4][t], res[1][4][t])
+        assert np.max(np.abs(res[0][3][t] - Ct[-1])) <= TOL * np.max(np.abs(Ct[-1]))
+        assert np.max(np.abs(res[0][4][t] - dC)) <= TOL * np.max(np.abs(dC))
+        gWt = np.concatenate([res[r][5][t] for r in range(world)])
+        gdW = np.concatenate([res[r][6][t] for r in range(world)])
+        assert np.max(np.abs(gWt - Wt)) <= TOL * np.max(np.abs(Wt))
+        assert np.max(np.abs(gdW - dWr)) <= TOL * np.max(np.abs(dWr))
