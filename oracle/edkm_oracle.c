@@ -27,9 +27,9 @@
  * Lloyd k-means; tau->inf and k=1 closed forms; scale law; permutation
  * invariance; backward vs torch fp64 autograd of an independently written
  * graph and vs central finite differences; table form vs dense form;
- * hard assignment vs brute force.  Parity is pinned for every function
- * except the eps-stopping rule (R4), whose iteration count only
- * self-consistency checks: "parity unpinned" for the eps > 0 stop decision.
+ * hard assignment vs brute force; the eps > 0 stop (R4) against textbook
+ * Lloyd k-means in exact rational arithmetic at tau = 1e-9.  Parity is pinned
+ * for every function.
  */
 #include <math.h>
 #include <pthread.h>

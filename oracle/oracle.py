@@ -17,8 +17,8 @@ Functions follow PAPER.md and DESIGN.md readings:
   dkm_backward_table  P:77 table form -- (phi, psi) per pattern, dC_0
   hard_assign    P:31, R9 -- nearest centroid, lowest index on ties
 
-The eps > 0 stopping decision (R4) is "parity unpinned": only
-self-consistency tests cover it.
+The eps > 0 stopping decision (R4) is pinned against textbook Lloyd k-means
+in exact rational arithmetic (tests/test_oracle.py::test_eps_stop_pinned_to_lloyd).
 """
 from __future__ import annotations
 

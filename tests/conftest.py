@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """EDKM_PARITY_REPORT=path: the normwise errors every GPU parity check measured, as JSON
+    (max and median per quantity, and every sample) -- DESIGN.md S7's measured error distribution."""
+    path = os.environ.get("EDKM_PARITY_REPORT")
+    mod = sys.modules.get("test_gpu_parity") or sys.modules.get("tests.test_gpu_parity")
+    if not path or mod is None or not getattr(mod, "ERRS", None):
+        return
+    import json
+    import statistics
+    by = {}
+    for test, q, v in mod.ERRS:
+        by.setdefault(q, []).append((v, test))
+    out = {q: {"n": len(v), "max": max(x for x, _ in v), "median": statistics.median(x for x, _ in v),
+               "worst_test": max(v)[1]} for q, v in by.items()}
+    with open(path, "w") as f:
+        json.dump({"summary": out, "samples": mod.ERRS}, f, indent=1)

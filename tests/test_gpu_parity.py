@@ -9,6 +9,8 @@ Bars (DESIGN.md "Parity"):
 The oracle runs dense over all |W| x |C| entries (CFG1 sizes) or, at full
 BASELINE sizes, in its pinned attention-table form from exact CPU counts.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -23,6 +25,13 @@ TOL = 1e-5
 # factor 2^26 between it and the GPU's fp32 flush-to-zero level 2^-126 per attention entry, so
 # above it the flushed entries change S_s[j] by < 2^-26 relative and every value is compared.
 DEAD = 2.0 ** -100
+
+
+ERRS = []  # (test, quantity, value): written to $EDKM_PARITY_REPORT by conftest (measured error distribution)
+
+
+def record(quantity, value):
+    ERRS.append((os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], quantity, float(value)))
 
 
 def bits_of(t: torch.Tensor) -> np.ndarray:
@@ -141,6 +150,7 @@ def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
         assert normwise(gpu["ctraj"][t][s], ref["Ct"][s]) <= TOL, ("C_s", s)
     for s in range(ref["T"]):
         assert normwise(gpu["straj"][t][s], ref["St"][s]) <= TOL, ("S_s", s)
+    record("C_T", normwise(gpu["C"][t], CT))
     assert normwise(gpu["C"][t], CT) <= TOL, ("C", normwise(gpu["C"][t], CT))
     # table for every populated finite pattern
     u = np.nonzero(gpu["counts"][t])[0]
@@ -151,6 +161,12 @@ def check_tensor(gpu, t, w_bits, G, ref, p: E.Params, dense=True):
         return
     Wt_ref, dW_ref = ref["Wt"], ref["dW"]
     assert np.all(np.isnan(gpu["Wt"][t][~fin])) and np.all(np.isnan(gpu["dW"][t][~fin]))
+    record("W~ fp32", normwise(gpu["Wt"][t][fin], Wt_ref[fin]))
+    record("dW fp32", normwise(gpu["dW"][t][fin], dW_ref[fin]))
+    record("dC_0", normwise(gpu["dC0"][t], ref["dC"]))
+    if fin.any():
+        record("W~ 16-bit ulps", float(np.max(np.abs(gpu["Wt16"][t][fin] - Wt_ref[fin]) / ulp16(Wt_ref[fin], p.wdtype))))
+        record("dW 16-bit ulps", float(np.max(np.abs(gpu["dW16"][t][fin] - dW_ref[fin]) / ulp16(dW_ref[fin], p.wdtype))))
     assert normwise(gpu["Wt"][t][fin], Wt_ref[fin]) <= TOL, ("Wt", normwise(gpu["Wt"][t][fin], Wt_ref[fin]))
     assert normwise(gpu["dW"][t][fin], dW_ref[fin]) <= TOL, ("dW", normwise(gpu["dW"][t][fin], dW_ref[fin]))
     # dC_0 normwise; its floor is set by the size of the summands (~sum |G|), below which the

@@ -14,7 +14,7 @@ from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SHORT = [("f1_hist", "F1"), ("tf_kernel", "TF"), ("f2_gather", "F2"), ("b1_bucket", "B1"), ("tgamma", "TGAMMA"),
-         ("tb_kernel", "TB"), ("b2_dw", "B2")]
+         ("tb_kernel", "TB"), ("tb_split", "TB"), ("b2_dw", "B2")]
 ALG = {"F1": 2, "F2": 4, "B1": 4, "B2": 6}
 FULL_METRICS = [
     ("gpu__time_duration.sum", "time"), ("dram__bytes_read.sum", "dram_read"), ("dram__bytes_write.sum", "dram_write"),
