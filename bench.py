@@ -284,7 +284,11 @@ def main():
     n_local = sum(numels)
     n_total = wl.numel
     # N > 1: split the table phase by tensor block when it is heavy (k T >= 64, e.g. CFG4's k=16, T=30):
-    # each rank runs TF/TB for its block, the ranks all-gather the per-tensor results (dist.ShardedStep)
+    # each rank runs TF/TB for its block and derives the other tensors' layout from the global counts;
+    # the ranks exchange the owners' states, trajectories and the populated pages of their tables
+    # (dist.ShardedStep(compact_tables=True)).  CFG3 (k T = 40) stays replicated by default: at N = 8
+    # the estimated split (own block TF + TB ~0.18 ms, layout pass ~0.03, five all-gathers ~0.1) saves
+    # ~0.04 ms of ~0.38; EDKM_SHARD_TABLE=1 forces the split, 0 disables it.
     tmode = os.environ.get("EDKM_SHARD_TABLE", "auto")
     shard = tmode == "1" or (world > 1 and tmode == "auto" and wl.k * wl.max_iter >= 64)
     if shard:
@@ -374,6 +378,12 @@ def main():
             nv = None
             plan.counts = torch.empty((plan.nt, E.PATTERNS), dtype=torch.int32, device=dev)
 
+    from paper_2309_00964_b200.dist import ShardedStep
+    # the page-exchange helper of the compact table split (the step below drives the calls itself so
+    # that it can record events between them)
+    ss = ShardedStep(plan, allreduce=lambda t: allreduce(t), allgather=lambda t: allgather(t),
+                     allreduce_max=allreduce_max, shard_table=shard, compact_tables=shard and compact)
+
     def step(ev=None):
         # the seven kernels of the hot path, one C-ABI call each, events between them
         def mark(i):
@@ -387,14 +397,23 @@ def main():
             plan.uniquify(Ws)                # F1
             mark(1)
             if compact:                      # exchange 1 (N > 1), populated pages only
-                exchange_counts_compact(plan, allreduce, allreduce_max)
+                ss.page_list = exchange_counts_compact(plan, allreduce, allreduce_max)
             else:
                 allreduce(plan.counts)       # exchange 1 (N > 1)
         mark(2)
         if shard:
             plan.forward_range(t0, t1, C0)   # TF, this rank's tensor block
-            for name in ("state", "ctraj", "rows", "page_cnt", "C_out", "table16"):
-                allgather(views[name])
+            if compact and nv is None:       # others: layout locally, owners' states + populated pages
+                if t0 > 0:
+                    plan.forward_layout_range(0, t0)
+                if t1 < plan.nt:
+                    plan.forward_layout_range(t1, plan.nt)
+                for name in ("state", "ctraj", "C_out"):
+                    allgather(views[name])
+                ss._exchange_pages("table16")
+            else:
+                for name in ("state", "ctraj", "rows", "page_cnt", "C_out", "table16"):
+                    allgather(views[name])
         else:
             plan.forward(C0)                 # TF
         mark(3)
@@ -408,8 +427,12 @@ def main():
         mark(7)
         if shard:
             plan.backward_table_range(t0, t1)  # TB, this rank's tensor block
-            for name in ("phipsi", "dC0"):
-                allgather(views[name])
+            if compact and nv is None:
+                ss._exchange_pages("phipsi")
+                allgather(views["dC0"])
+            else:
+                for name in ("phipsi", "dC0"):
+                    allgather(views[name])
         else:
             plan.backward_table()            # TB
         mark(8)
@@ -442,6 +465,9 @@ def main():
         allreduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     launches_per_step = 7 + (nv is not None) + 3 * (compact and nv is None)  # + NVLS barrier / page exchange
+    if shard and compact and nv is None:  # TF layout passes + page packs / unpacks of table16 and (phi, psi)
+        lists = ss._pg_cache["lists"][1]
+        launches_per_step += int(t0 > 0) + int(t1 < plan.nt) + 2 * sum(1 for x in lists if x.numel())
     # N > 1: C_T and dC_0 must be bit-identical on every rank ("weights are identical in each
     # learner"): all-gather a hash of their bytes and fail on any mismatch
     rank_identical = None
@@ -556,7 +582,9 @@ def main():
                                f"b={wl.bits} (k={wl.k}), tau={wl.tau}, T={wl.max_iter}",
                    "tensors": len(wl.shapes), "weights": n_total, "bits": wl.bits, "tau": wl.tau,
                    "iters": wl.max_iter, "parallelism": f"slices{world}", "exchange": exchange,
-                   "table_phase": "split by tensor block + all-gather" if shard else "replicated on every rank",
+                   "table_phase": ("split by tensor block + " + ("page-compact exchange" if compact and nv is None
+                                                                  else "all-gather") if shard
+                                   else "replicated on every rank"),
                    "arith": f"{w16} I/O; exact integer F1/B1 sums, fp32 B2 FMA; fp64 table phase",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
         "phases_ms": phase, "gpu_launches": launches_per_step * args.steps, "rank_identical_C_dC0": rank_identical,

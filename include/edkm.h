@@ -197,6 +197,15 @@ edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, co
 edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p, const float* C0,
                                float* C_out, float* table, void* saved, void* stream);
 
+/* TF's layout part only, for tensors [t0, t1): the populated-pattern rows and partitions, the page
+ * masses, the non-finite counts, the per-weight kernels' windows (all in `saved`) and the NaN fill
+ * of the W~ tables -- everything every rank derives identically from the global counts -- but no
+ * iterations, no C trajectory and no W~ values.  For a table phase split by tensor (the rank that
+ * does not own a tensor then receives only its C trajectory, TensorState, C_T and the populated
+ * pages of its tables; dist.ShardedStep(compact_tables=True)).  table: [nt][65536] fp32. */
+edkm_status edkm_forward_layout_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p,
+                                      float* table, void* saved, void* stream);
+
 /* Byte offsets of the arrays inside `saved` and `ws` for nt tensors (for exchanging per-tensor
  * blocks between ranks).  Each array is [nt][per-tensor entries], tensor-major.
  *   saved_offs[8] : TensorState (144 B/tensor), C trajectory (fp64 (max_iter+1)k), S trajectory
@@ -305,6 +314,15 @@ edkm_status edkm_counts_pack(const int32_t* counts, int nt, const int32_t* pages
                              void* stream);
 edkm_status edkm_counts_unpack(const int32_t* compact, const int32_t* pages, int npages, int nt, int32_t* counts,
                                void* stream);
+/* The same page copy for any per-pattern table of nt tensors with entries of esize bytes (1, 2, 4
+ * or 8: idx8, table16, the fp32 W~ table, (phi, psi)): pack gathers pages pages[i] of `table` into
+ * compact[i][0..256 esize), unpack scatters them back.  Both buffers 16-byte aligned.  Used to
+ * exchange only the populated pages of the per-pattern tables when the table phase is split by
+ * tensor (dist.ShardedStep(compact_tables=True)). */
+edkm_status edkm_pages_pack(const void* table, int esize, int nt, const int32_t* pages, int npages, void* compact,
+                            void* stream);
+edkm_status edkm_pages_unpack(const void* compact, int esize, const int32_t* pages, int npages, int nt, void* table,
+                              void* stream);
 
 /* Copies per-tensor status to host and synchronises `stream`:
  *   nonfinite_host[t] = number of weights of tensor t whose pattern is NaN/Inf (global),

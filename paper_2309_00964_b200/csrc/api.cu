@@ -296,6 +296,27 @@ edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, co
   return EDKM_OK;
 }
 
+edkm_status edkm_forward_layout_range(const int32_t* counts, int nt, int t0, int t1, const edkm_params* p,
+                                      float* table, void* saved, void* stream) {
+  EDKM_NVTX("edkm TF layout");
+  g_launches = 0;
+  edkm_status st = check_params(p);
+  if (st != EDKM_OK) return st;
+  if (nt < 0) return fail(EDKM_E_ARG, "nt < 0");
+  if (t0 < 0 || t1 < t0 || t1 > nt) return fail(EDKM_E_ARG, "tensor range outside [0, nt]");
+  if (t1 == t0) return EDKM_OK;
+  if (!counts || !table || !saved) return fail(EDKM_E_ARG, "NULL buffer");
+  TableArgs P = table_args(nt, p, saved);
+  P.counts = counts;
+  P.table = table;
+  P.layout_only = 1;
+  const TableArgs R = table_range(P, t0, t1);
+  cudaError_t e = R.k >= 32 ? launch_tf_wide(R, (cudaStream_t)stream) : launch_tf(R, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "TF layout launch");
+  g_launches = 1;
+  return EDKM_OK;
+}
+
 edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
                          float* table, void* saved, void* stream) {
   if (nt < 0) {

@@ -104,19 +104,22 @@ __global__ void count_pages_kernel(const int32_t* __restrict__ counts, int64_t n
   }
 }
 
-// DIR 0: compact[i] = counts page pages[i]; DIR 1: counts page pages[i] = compact[i].
-// One 64-thread group per page (one int4 per thread), grid-stride over the page list.
+// DIR 0: compact[i] = page pages[i] of the table; DIR 1: page pages[i] of the table = compact[i].
+// A page is 256 entries of `esize` bytes (q16 = 16 * esize int4 words).  One 64-thread group per
+// page, grid-stride over the page list; a page id outside [0, npages_table) is skipped.
 template <int DIR>
-__global__ void page_copy_kernel(int32_t* __restrict__ counts, const int32_t* __restrict__ pages, int npages,
-                                 int32_t* __restrict__ compact, int64_t ncount_pages) {
+__global__ void page_copy_kernel(int4* __restrict__ table, const int32_t* __restrict__ pages, int npages,
+                                 int4* __restrict__ compact, int64_t npages_table, int q16) {
   const int per = blockDim.x >> 6;
   for (int i = blockIdx.x * per + (threadIdx.x >> 6); i < npages; i += gridDim.x * per) {
     const int32_t pg = __ldg(pages + i);
-    if (pg < 0 || pg >= ncount_pages) continue;  // a bad page id is skipped, never a stray access
-    int4* c = reinterpret_cast<int4*>(counts + (int64_t)pg * 256) + (threadIdx.x & 63);
-    int4* k = reinterpret_cast<int4*>(compact + (int64_t)i * 256) + (threadIdx.x & 63);
-    if (DIR == 0) *k = *c;
-    else *c = *k;
+    if (pg < 0 || pg >= npages_table) continue;
+    int4* c = table + (int64_t)pg * q16;
+    int4* k = compact + (int64_t)i * q16;
+    for (int q = threadIdx.x & 63; q < q16; q += 64) {
+      if (DIR == 0) k[q] = c[q];
+      else c[q] = k[q];
+    }
   }
 }
 
@@ -229,16 +232,21 @@ edkm_status edkm_count_pages(const int32_t* counts, int nt, uint8_t* mask, void*
   return EDKM_OK;
 }
 
-static edkm_status page_copy(int dir, int32_t* counts, int nt, const int32_t* pages, int npages, int32_t* compact,
+static edkm_status page_copy(int dir, void* table, int esize, int nt, const int32_t* pages, int npages, void* compact,
                              void* stream) {
   reset_launches();
-  if (nt < 0 || npages < 0 || npages > nt * 256) return set_error(EDKM_E_ARG, "need 0 <= npages <= 256 nt");
+  if (esize != 1 && esize != 2 && esize != 4 && esize != 8) return set_error(EDKM_E_ARG, "esize must be 1, 2, 4 or 8");
+  if (nt < 0 || npages < 0 || (int64_t)npages > (int64_t)nt * 256) return set_error(EDKM_E_ARG, "need 0 <= npages <= 256 nt");
   if (npages == 0) return EDKM_OK;
-  if (!counts || !pages || !compact) return set_error(EDKM_E_ARG, "NULL buffer");
+  if (!table || !pages || !compact) return set_error(EDKM_E_ARG, "NULL buffer");
+  if (((uintptr_t)table | (uintptr_t)compact) & 15u) return set_error(EDKM_E_ARG, "buffers must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t ncp = (int64_t)nt * 256;
-  if (dir == 0) page_copy_kernel<0><<<grid_pages(npages, 4), 256, 0, s>>>(counts, pages, npages, compact, ncp);
-  else page_copy_kernel<1><<<grid_pages(npages, 4), 256, 0, s>>>(counts, pages, npages, compact, ncp);
+  const int q16 = 16 * esize;
+  int4* t4 = reinterpret_cast<int4*>(table);
+  int4* c4 = reinterpret_cast<int4*>(compact);
+  if (dir == 0) page_copy_kernel<0><<<grid_pages(npages, 4), 256, 0, s>>>(t4, pages, npages, c4, ncp, q16);
+  else page_copy_kernel<1><<<grid_pages(npages, 4), 256, 0, s>>>(t4, pages, npages, c4, ncp, q16);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(EDKM_E_CUDA, cudaGetErrorString(e));
   add_launches(1);
@@ -247,12 +255,22 @@ static edkm_status page_copy(int dir, int32_t* counts, int nt, const int32_t* pa
 
 edkm_status edkm_counts_pack(const int32_t* counts, int nt, const int32_t* pages, int npages, int32_t* compact,
                              void* stream) {
-  return page_copy(0, const_cast<int32_t*>(counts), nt, pages, npages, compact, stream);
+  return page_copy(0, const_cast<int32_t*>(counts), 4, nt, pages, npages, compact, stream);
 }
 
 edkm_status edkm_counts_unpack(const int32_t* compact, const int32_t* pages, int npages, int nt, int32_t* counts,
                                void* stream) {
-  return page_copy(1, counts, nt, pages, npages, const_cast<int32_t*>(compact), stream);
+  return page_copy(1, counts, 4, nt, pages, npages, const_cast<int32_t*>(compact), stream);
+}
+
+edkm_status edkm_pages_pack(const void* table, int esize, int nt, const int32_t* pages, int npages, void* compact,
+                            void* stream) {
+  return page_copy(0, const_cast<void*>(table), esize, nt, pages, npages, compact, stream);
+}
+
+edkm_status edkm_pages_unpack(const void* compact, int esize, const int32_t* pages, int npages, int nt, void* table,
+                              void* stream) {
+  return page_copy(1, table, esize, nt, pages, npages, const_cast<void*>(compact), stream);
 }
 
 }  // extern "C"

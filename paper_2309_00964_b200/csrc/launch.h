@@ -79,6 +79,7 @@ cudaError_t launch_b2(const StreamArgs& A, const B2Args& B, int sms, cudaStream_
 // ---- table phase
 struct TableArgs {
   int nt, k, wdtype, max_iter, cl;
+  int layout_only;         // TF: rows, partitions, page masses, windows only (no iterations, no tables)
   double tau, inv_tau, eps;
   const int32_t* counts;   // [nt][65536]
   const float* C0;         // [nt][k]

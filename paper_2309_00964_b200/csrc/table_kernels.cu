@@ -327,6 +327,11 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
       for (int r = 0; r <= cl; ++r) st->pbase[r] = s_pb[r];
     }
   }
+  if (P.layout_only) {  // a rank that does not own this tensor: its layout, from the global counts
+    cluster.sync();
+    table_windows(P.page_cnt + (int64_t)t * 256, st, crank);
+    return;
+  }
   RowStage R{rows, cnt, reinterpret_cast<float*>(stage_mem), reinterpret_cast<int32_t*>(stage_mem) + kStage, nullptr,
              nullptr, nr, P.wdtype, kStage};
   R.stage();

@@ -186,6 +186,11 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
       for (int r = 0; r <= cl; ++r) st->pbase[r] = s_pb[r];
     }
   }
+  if (P.layout_only) {  // a rank that does not own this tensor: its layout, from the global counts
+    cluster.sync();
+    table_windows(P.page_cnt + (int64_t)t * 256, P.state + t, crank);
+    return;
+  }
   for (int r = tid; r < nr && r < kWStage; r += kWThreads) {
     const uint32_t u = rows[r];
     S.sv[r] = decode16(u, P.wdtype);

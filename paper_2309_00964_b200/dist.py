@@ -72,14 +72,16 @@ def exchange_counts_compact(k, allreduce_sum_fn, allreduce_max_fn):
     """Sum the ranks' counts over the union of their populated pages only.
 
     `k` has the Plan interface (counts, count_pages, pack_counts, unpack_counts).  Pages that no rank
-    populated are zero on every rank, so after this every rank holds the exact global counts."""
+    populated are zero on every rank, so after this every rank holds the exact global counts.
+    Returns the union's global page ids t*256 + p (host int32, ascending)."""
     mask = k.count_pages()
     allreduce_max_fn(mask)
-    pages = union_pages(mask).to(k.counts.device)
+    host = union_pages(mask)
+    pages = host.to(k.counts.device)
     compact = k.pack_counts(pages)
     allreduce_sum_fn(compact)
     k.unpack_counts(pages, compact)
-    return pages.numel()
+    return host
 
 
 def padded_numels(numels, world: int):
@@ -106,6 +108,11 @@ class ShardedStep:
     reconstruct, backward_reduce, backward_apply, counts, gamma, dC0); on a
     B200 it is paper_2309_00964_b200.edkm.Plan.
 
+    compact_tables=True (with shard_table; implies the page-compact count exchange): ranks derive
+    the tensors they do not own from the global counts (edkm_forward_layout_range: rows, windows)
+    and exchange only the owners' C trajectories, states, C_T and the union pages of the W~ and
+    (phi, psi) tables (edkm_pages_pack / _unpack) -- ~8x less than whole tables for CFG3.
+
     shard_table=True splits the table phase by tensor block: rank r runs
     TF and TB only for tensors [r nt/P, (r+1) nt/P) (edkm_forward_range / _backward_table_range)
     and the ranks all-gather the per-tensor results the per-weight kernels need -- after TF the
@@ -116,23 +123,26 @@ class ShardedStep:
     """
 
     def __init__(self, kernels, group=None, allreduce=None, nvls=None, shard_table=False, allgather=None,
-                 out_mode="all", comm=None, compact_counts=False):
+                 out_mode="all", comm=None, compact_counts=False, compact_tables=False, allreduce_max=None):
         self.k = kernels
         self.group = group
         self.comm = comm
         if comm is not None:
             self.allreduce = allreduce or (lambda t: comm.allreduce(t))
-            self.allreduce_max = lambda t: comm.allreduce(t, op=1)
+            self.allreduce_max = allreduce_max or (lambda t: comm.allreduce(t, op=1))
             self.allgather = allgather or (lambda t: comm.allgather_blocks(t))
         else:
             self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
-            self.allreduce_max = lambda t: allreduce_max(t, self.group)
+            self.allreduce_max = allreduce_max or (lambda t: globals()["allreduce_max"](t, self.group))
             self.allgather = allgather or (lambda t: allgather_blocks(t, self.group))
         self.nvls = nvls
         self.shard_table = shard_table
         self.out_mode = out_mode
-        self.compact_counts = compact_counts
+        self.compact_counts = compact_counts or compact_tables
+        self.compact_tables = compact_tables
         self.pages_exchanged = None  # pages summed by the last compact count exchange
+        self.page_list = None        # their global ids t*256 + p (host int32), for compact_tables
+        self._pg_cache = {}          # per-rank page lists of the last union
 
     def _block(self):
         P = dist.get_world_size(self.group) if dist.is_initialized() else 1
@@ -147,7 +157,8 @@ class ShardedStep:
             self.k.uniquify_nvls(weights, self.nvls)      # exchange 1 fused into F1 (NVSwitch)
         elif self.compact_counts:
             self.k.uniquify(weights)                      # exchange 1, populated pages only
-            self.pages_exchanged = exchange_counts_compact(self.k, self.allreduce, self.allreduce_max)
+            self.page_list = exchange_counts_compact(self.k, self.allreduce, self.allreduce_max)
+            self.pages_exchanged = int(self.page_list.numel())
         elif self.comm is not None:
             self.k.uniquify(weights, comm=self.comm)      # exchange 1 inside edkm_uniquify
         else:
@@ -165,20 +176,62 @@ class ShardedStep:
             return self.k.dC0
         t0, t1 = self._block()
         v = self.k.views()
+        tables = {"16": ["table16"], "fp32": ["table"]}.get(self.out_mode, ["table16", "table", "idx8"])
         self.k.forward_range(t0, t1, C0)                  # TF, own tensor block
-        names = ["state", "ctraj", "rows", "page_cnt", "C_out"]
-        names += {"16": ["table16"], "fp32": ["table"]}.get(self.out_mode, ["table16", "table", "idx8"])
-        for n in names:
-            self.allgather(v[n])
+        if self.compact_tables:
+            # the other tensors' layout from the global counts (identical on every rank), then only
+            # the owners' C trajectories, states, C_T and the populated pages of their tables
+            if t0 > 0:
+                self.k.forward_layout_range(0, t0)
+            if t1 < self.k.nt:
+                self.k.forward_layout_range(t1, self.k.nt)
+            for n in ("state", "ctraj", "C_out"):
+                self.allgather(v[n])
+            for n in tables:
+                self._exchange_pages(n)
+        else:
+            for n in ["state", "ctraj", "rows", "page_cnt", "C_out"] + tables:
+                self.allgather(v[n])
         self.k.reconstruct(weights, outs)
         self.k.backward_buckets(weights, grads)
         self.k.backward_gamma()
         self.allreduce(self.k.gamma)                      # exchange 2: gamma_T partials
         self.k.backward_table_range(t0, t1)               # TB, own tensor block
-        for n in ("phipsi", "dC0"):
-            self.allgather(v[n])
+        if self.compact_tables:
+            self._exchange_pages("phipsi")
+            self.allgather(v["dC0"])
+        else:
+            for n in ("phipsi", "dC0"):
+                self.allgather(v[n])
         self.k.backward_dw(weights, grads, dW)
         return self.k.dC0
+
+    def _exchange_pages(self, name):
+        """All-gather of the populated pages of each rank's tensor block of the per-pattern table
+        `name` (a views() array): rank r packs the union pages of tensors [r b, (r+1) b) into rows
+        [r m, r m + n_r) of one [P m][page bytes] buffer (m = the largest n_r), the buffer is
+        all-gathered and every other rank's rows are unpacked (edkm_pages_pack / _unpack)."""
+        P = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        r = dist.get_rank(self.group) if dist.is_initialized() else 0
+        b = self.k.nt // P
+        v = self.k.views()[name]
+        pb = v.shape[1] // 256  # bytes per page
+        hit = self._pg_cache.get("lists")
+        if hit is None or not torch.equal(hit[0], self.page_list):  # per-rank lists of this step's union
+            owner = self.page_list.long() // (256 * b)
+            lists = [self.page_list[owner == q] for q in range(P)]
+            m = max(1, max(int(x.numel()) for x in lists))
+            dev = self.k.counts.device
+            hit = (self.page_list.clone(), [x.to(dev) for x in lists], m)
+            self._pg_cache["lists"] = hit
+        _, lists, m = hit
+        full = torch.empty((P * m, pb), dtype=torch.uint8, device=self.k.counts.device)
+        if lists[r].numel():
+            self.k.pack_pages(name, lists[r], full[r * m:r * m + lists[r].numel()])
+        self.allgather(full)
+        for q in range(P):
+            if q != r and lists[q].numel():
+                self.k.unpack_pages(name, lists[q], full[q * m:q * m + lists[q].numel()])
 
 
 class NvlsUnavailable(RuntimeError):

@@ -113,6 +113,9 @@ def lib():
             "edkm_count_pages": ([P, i32, P, P], i32),
             "edkm_counts_pack": ([P, i32, P, i32, P, P], i32),
             "edkm_counts_unpack": ([P, P, i32, i32, P, P], i32),
+            "edkm_pages_pack": ([P, i32, i32, P, i32, P, P], i32),
+            "edkm_pages_unpack": ([P, i32, P, i32, i32, P, P], i32),
+            "edkm_forward_layout_range": ([P, i32, i32, i32, pp, P, P, P], i32),
             "edkm_status_string": ([i32], ctypes.c_char_p),
             "edkm_last_error": ([], ctypes.c_char_p),
         }
@@ -133,7 +136,8 @@ def exported_symbols() -> list:
             "edkm_mc_supported", "edkm_mc_create", "edkm_mc_import", "edkm_mc_bytes", "edkm_mc_add_device",
             "edkm_mc_bind", "edkm_mc_destroy", "edkm_mc_last_error", "edkm_comm_unique_id", "edkm_comm_init",
             "edkm_comm_destroy", "edkm_comm_info", "edkm_comm_allreduce", "edkm_comm_allgather", "edkm_count_pages",
-            "edkm_counts_pack", "edkm_counts_unpack", "edkm_ipc_handle", "edkm_ipc_open", "edkm_ipc_close"]
+            "edkm_counts_pack", "edkm_counts_unpack", "edkm_ipc_handle", "edkm_ipc_open", "edkm_ipc_close",
+            "edkm_pages_pack", "edkm_pages_unpack", "edkm_forward_layout_range"]
 
 
 def _check(rc: int, what: str):
@@ -478,6 +482,27 @@ class Plan:
                                         _ptr(self.C_out), _ptr(self.table), _ptr(self.saved), _stream(stream)),
                "edkm_forward_range")
         return self.C_out
+
+    def forward_layout_range(self, t0, t1, stream=None):
+        """TF's layout part only for tensors [t0, t1) (edkm_forward_layout_range)."""
+        _check(lib().edkm_forward_layout_range(_ptr(self.counts), self.nt, t0, t1, ctypes.byref(self.p.c()),
+                                               _ptr(self.table), _ptr(self.saved), _stream(stream)),
+               "edkm_forward_layout_range")
+
+    def pack_pages(self, name, pages: torch.Tensor, out: torch.Tensor, stream=None):
+        """The listed pages of the per-pattern table `name` (a views() array) into `out` (edkm_pages_pack)."""
+        v = self.views()[name]
+        es = v.shape[1] // 65536
+        _check(lib().edkm_pages_pack(_ptr(v), es, self.nt, _ptr(pages), pages.numel(), _ptr(out), _stream(stream)),
+               "edkm_pages_pack")
+        return out
+
+    def unpack_pages(self, name, pages: torch.Tensor, src: torch.Tensor, stream=None):
+        """The listed pages of the per-pattern table `name` = src (edkm_pages_unpack)."""
+        v = self.views()[name]
+        es = v.shape[1] // 65536
+        _check(lib().edkm_pages_unpack(_ptr(src), es, _ptr(pages), pages.numel(), self.nt, _ptr(v), _stream(stream)),
+               "edkm_pages_unpack")
 
     def backward_table_range(self, t0, t1, stream=None):
         """TB for tensors [t0, t1) only (edkm_backward_table_range)."""

@@ -121,7 +121,7 @@ def _compact_worker(rank, world, port, q):
         kern = OracleKernels(len(sizes), K)
         kern.uniquify([w[a:b].contiguous() for w, (a, b) in zip(Ws, rng)])
         local_pages = int(kern.count_pages().sum())
-        npages = exchange_counts_compact(kern, allreduce_sum, allreduce_max)
+        npages = int(exchange_counts_compact(kern, allreduce_sum, allreduce_max).numel())
         q.put((rank, kern.counts.numpy().copy(), npages, local_pages))
     finally:
         dist.destroy_process_group()

@@ -40,6 +40,13 @@ def _gather_via_host(t: torch.Tensor):
     t.copy_(torch.cat(parts).to(t.device))
 
 
+def _max_via_host(t: torch.Tensor):
+    from paper_2309_00964_b200.dist import allreduce_max
+    h = t.cpu()
+    allreduce_max(h)
+    t.copy_(h)
+
+
 def _worker(rank, world, port, q, shard_table=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,8 +68,11 @@ def _worker(rank, world, port, q, shard_table=False):
         plan = E.Plan(numels, p, dev)
         outs = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
         dW = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
-        ShardedStep(plan, allreduce=_reduce_via_host, allgather=_gather_via_host, shard_table=shard_table,
-                    out_mode="fp32")(Wl, Gl, C0, outs, dW)
+        compact = shard_table == "compact"
+        step = ShardedStep(plan, allreduce=_reduce_via_host, allgather=_gather_via_host, shard_table=bool(shard_table),
+                           out_mode="fp32", compact_tables=compact, allreduce_max=_max_via_host)
+        for _ in range(2 if compact else 1):  # twice: the second step reuses the cached page lists
+            step(Wl, Gl, C0, outs, dW)
         torch.cuda.synchronize()
         q.put((rank, plan.counts.cpu().numpy(), plan.C_out.cpu().numpy(), plan.dC0.cpu().numpy(),
                [o.cpu().double().numpy() for o in outs], [d.cpu().double().numpy() for d in dW]))
@@ -78,10 +88,12 @@ def free_port():
     return port
 
 
-@pytest.mark.parametrize("shard_table", [False, True])
+@pytest.mark.parametrize("shard_table", [False, True, "compact"])
 def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table):
     """shard_table=True: each rank runs TF/TB for its own tensor block and the ranks all-gather
-    the per-tensor results (SURVEY S8(f) NEXT #2); results must be the same."""
+    the per-tensor results; "compact": the other tensors' layout is derived
+    locally and only the owners' states, trajectories and populated table pages are exchanged.
+    Results must be the same."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
