@@ -84,6 +84,15 @@ def test_comm_and_exchange_arguments(L):
     assert L.edkm_counts_pack(None, 1, None, 0, None, None) == 0
     assert L.edkm_counts_unpack(None, None, 3, 1, None, None) == 1
     assert L.edkm_status_string(5).startswith(b"EDKM_E_NCCL")
+    assert L.edkm_pages_pack(None, 3, 1, None, 1, None, None) == 1                 # esize not 1/2/4/8
+    assert L.edkm_pages_pack(None, 8, 1, None, 0, None, None) == 0
+    assert L.edkm_pages_unpack(None, 2, None, 300, 1, None, None) == 1             # npages > 256 nt
+    assert L.edkm_pages_pack(ctypes.c_void_p(8), 2, 1, ctypes.c_void_p(16), 1, ctypes.c_void_p(16), None) == 1  # misaligned
+    p = E.Params()
+    assert L.edkm_forward_layout_range(None, 2, 1, 3, ctypes.byref(p.c()), None, None, None) == 1  # range outside
+    assert L.edkm_forward_layout_range(None, 2, 1, 1, ctypes.byref(p.c()), None, None, None) == 0  # empty range
+    assert L.edkm_ipc_handle(None, None, None) == 1
+    assert L.edkm_ipc_close(None) == 0
 
 
 def test_empty_calls_are_noops(L):
