@@ -429,6 +429,67 @@ __device__ __forceinline__ void f1_body(const StreamArgs& A, int32_t* counts, ui
   }
 }
 
+// ---------------------------------------------------------------- F1 for fp16 weights
+// fp16 N(0, 0.02^2) weights spread over quarter-binade pages: the lane-private window (7 pages)
+// holds about half of them, so fp16 segments always took f1_body's shared-array path -- whose
+// per-element range test and branch (patterns >= 0xE000 go to the L2 counts) issued ~3x the
+// instructions of the atomic itself.  This kernel runs that path alone (the bf16 kernel keeps its
+// register allocation), branch-free: every pattern is clamped to the trash counter h[kF1Bins]
+// (never flushed) and a vector holding one >= 0xE000 (|w| >= 512: not in trained weights) re-adds
+// those to the global counts.  Still bound by shared-atomic bank conflicts (~7.7 wavefronts per
+// warp instruction: DESIGN S9).
+template <int MC>
+struct F1SharedPolicy : F1Policy<MC> {
+  static constexpr int kLoop = 0;
+  using typename F1Policy<MC>::Vec;
+  __device__ void begin(int t, int64_t a, int64_t b) {
+    if (threadIdx.x == 0) this->h[kF1Bins] = 0;  // the trash counter (never read; initialised for initcheck)
+    F1Policy<MC>::begin(t, a, b);
+  }
+  __device__ void process(int t, int64_t i, const Vec& r) {
+    const uint32_t base = smem_addr(this->h);
+    uint32_t mx2 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t x = r.w.x[q];
+      mx2 = __vmaxu2(mx2, x);
+      const uint32_t c2 = __vminu2(x, (uint32_t)kF1Bins * 0x10001u);
+      red_add_shared(base + (c2 & 0xFFFFu) * 4u, 1u);
+      red_add_shared(base + (c2 >> 16) * 4u, 1u);
+    }
+    if (max(mx2 & 0xFFFFu, mx2 >> 16) >= (uint32_t)kF1Bins) {
+      // rare: re-read the 16 patterns (dynamic indexing of the register vector would spill it)
+#pragma unroll 1
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t u = this->A.w[t][i + e];
+        if (u >= (uint32_t)kF1Bins) cnt_add<MC>(&this->cnt(t)[u], 1, this->A.peer_delta);
+      }
+    }
+  }
+};
+
+template <int MC>
+__global__ void __launch_bounds__(kThreads, 1) f1_fp16_kernel(const __grid_constant__ StreamArgs A, int32_t* counts,
+                                                              uint32_t* flags_mc) {
+  extern __shared__ __align__(16) uint32_t smem_u32[];
+  F1SharedPolicy<MC> p{{A, smem_u32, counts}};
+  for_each_segment(A, p);
+  if (MC) {  // NVLS arrival, as in f1_hist_kernel
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (MC == 1) {
+        asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+      } else {
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(flags_mc + blockIdx.x) : "memory");
+        if (A.peer_delta)
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(reinterpret_cast<char*>(flags_mc + blockIdx.x) +
+                                                                        A.peer_delta)
+                       : "memory");
+      }
+    }
+  }
+}
+
 // ============================================================================ F2
 // mode: 0 soft 16-bit, 1 hard-value 16-bit, 2 soft fp32, 3 hard-value fp32, 4 hard index u8
 
@@ -982,6 +1043,12 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 cudaError_t launch_f1(const StreamArgs& A, int32_t* counts, int sms, cudaStream_t s) {
   if (A.total == 0) return cudaSuccess;
   const size_t smem = kF1Smem;
+  if (A.wdtype == kFP16) {
+    cudaError_t e = set_smem((const void*)f1_fp16_kernel<0>, smem);
+    if (e != cudaSuccess) return e;
+    f1_fp16_kernel<0><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, nullptr);
+    return cudaGetLastError();
+  }
   cudaError_t e = set_smem((const void*)f1_hist_kernel<0>, smem);
   if (e != cudaSuccess) return e;
   f1_hist_kernel<0><<<grid_for(A.total, sms), kThreads, smem, s>>>(A, counts, 0x10000u, 128u, nullptr);
@@ -1007,11 +1074,18 @@ cudaError_t nvls_failed(int* failed) {
 cudaError_t launch_f1_nvls(const StreamArgs& A, int32_t* counts_mc, uint32_t* flags_mc, const uint32_t* flags,
                            uint32_t* epoch, int nranks, int emulate, int sms, cudaStream_t s) {
   const size_t smem = kF1Smem;
-  const void* fn = emulate ? (const void*)f1_hist_kernel<2> : (const void*)f1_hist_kernel<1>;
+  const bool h = A.wdtype == kFP16;
+  const void* fn = emulate ? (h ? (const void*)f1_fp16_kernel<2> : (const void*)f1_hist_kernel<2>)
+                           : (h ? (const void*)f1_fp16_kernel<1> : (const void*)f1_hist_kernel<1>);
   cudaError_t e = set_smem(fn, smem);
   if (e != cudaSuccess) return e;
-  if (emulate) f1_hist_kernel<2><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
-  else f1_hist_kernel<1><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
+  if (h) {
+    if (emulate) f1_fp16_kernel<2><<<sms, kThreads, smem, s>>>(A, counts_mc, flags_mc);
+    else f1_fp16_kernel<1><<<sms, kThreads, smem, s>>>(A, counts_mc, flags_mc);
+  } else {
+    if (emulate) f1_hist_kernel<2><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
+    else f1_hist_kernel<1><<<sms, kThreads, smem, s>>>(A, counts_mc, 0x10000u, 128u, flags_mc);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   f1_nvls_wait_kernel<<<1, 256, 0, s>>>(flags, sms, epoch, (uint32_t)nranks, (uint64_t)(g_nvls_timeout_s * 1e9),
