@@ -45,7 +45,7 @@ NcclApi load_nccl() {
   NcclApi a;
   memset(&a, 0, sizeof(a));
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's NCCL (torch's), if loaded
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);   // else the system's, kept private
   if (!h) {
     snprintf(a.why, sizeof(a.why), "cannot load libnccl.so.2: %s", dlerror());
     return a;
