@@ -103,6 +103,16 @@ struct CSet {
   }
 };
 
+#ifndef EDKM_TF_F2D_INT
+#define EDKM_TF_F2D_INT 2
+#endif
+// exact fp32 -> fp64 of a normal or zero non-negative float (an ex2.approx.ftz result) by integer
+// ops: exponent rebias (+896 << 20 in the high word) and the mantissa split over both words
+__device__ __forceinline__ double f2d_pos(float a) {
+  const uint32_t f = __float_as_uint(a);
+  return __hiloint2double((int)(f ? (f >> 3) + 0x38000000u : 0u), (int)(f << 29));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -385,8 +395,11 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
       const double nz = R.n(r) * (double)attention_row_raw<K>((float)v, cs, A), nvz = nz * v;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        acc[j] = fma((double)A[j], nz, acc[j]);
-        acc[K + j] = fma((double)A[j], nvz, acc[K + j]);
+        // every EDKM_TF_F2D_INT-th conversion by integer ops (f2d_pos), the others by F2F: the
+        // XU pipe carries both the exponentials and F2F.F64.F32
+        const double a = (EDKM_TF_F2D_INT && j % EDKM_TF_F2D_INT == 0) ? f2d_pos(A[j]) : (double)A[j];
+        acc[j] = fma(a, nz, acc[j]);
+        acc[K + j] = fma(a, nvz, acc[K + j]);
       }
     }
     cluster_allreduce<2 * K, kFThreads / 32>(acc, red, part, tot, it & 1, cluster);
