@@ -373,3 +373,42 @@ def test_nvls_protocol_two_writers_matches_oracle():
         gdW = np.concatenate([res[r][6][t] for r in range(world)])
         assert np.max(np.abs(gWt - Wt)) <= TOL * np.max(np.abs(Wt))
         assert np.max(np.abs(gdW - dWr)) <= TOL * np.max(np.abs(dWr))
+
+
+@pytest.mark.parametrize("dtype,bits", [(torch.bfloat16, 3), (torch.float16, 4), (torch.bfloat16, 6)])
+def test_forward_layout_range_matches_full_tf(dtype, bits):
+    """edkm_forward_layout_range (a non-owner's view of a tensor in the compact table split) writes the
+    same rows, partitions, page masses, non-finite counts and per-weight-kernel windows as the full TF,
+    from the counts alone."""
+    dev = torch.device("cuda")
+    sizes = [300_001, 65_536 + 3, 17, 0, 1_000_000]
+    p = E.Params(dtype, bits, 1e-3, 3)
+    Ws = [synth.normal_tensor(n, 0.02, dtype, 40 + i).to(dev) for i, n in enumerate(sizes)]
+    Ws[0][5] = float("nan")
+    C0 = torch.tensor([synth.quantile_centroids(p.k, 0.02)] * len(sizes), dtype=torch.float32, device=dev)
+    full, lay = E.Plan(sizes, p, dev), E.Plan(sizes, p, dev)
+    for pl in (full, lay):
+        pl.uniquify(Ws)
+    full.forward(C0)
+    lay.views()["state"].zero_()
+    lay.forward_layout_range(0, len(sizes))
+    torch.cuda.synchronize()
+    vf, vl = full.views(), lay.views()
+    st_f, st_l = vf["state"].cpu().numpy(), vl["state"].cpu().numpy()
+    assert torch.equal(vf["page_cnt"].cpu(), vl["page_cnt"].cpu())
+    for t in range(len(sizes)):
+        # TensorState (launch.h): T @0 is the owner's; cl @4, pbase[9] @8, nrows[8] @44, win[4] @76,
+        # nonfinite[8] (int64) @80 -- the first cl entries of each are defined
+        st, sl = st_f[t], st_l[t]
+        cl = int(st[4:8].view(np.int32)[0])
+        assert cl == int(sl[4:8].view(np.int32)[0])
+        pb = st[8:44].view(np.int32)
+        nr = st[44:76].view(np.int32)
+        assert np.array_equal(pb[:cl + 1], sl[8:44].view(np.int32)[:cl + 1])
+        assert np.array_equal(nr[:cl], sl[44:76].view(np.int32)[:cl])
+        assert np.array_equal(st[76:80], sl[76:80])
+        assert np.array_equal(st[80:144].view(np.int64)[:cl], sl[80:144].view(np.int64)[:cl])
+        rf = vf["rows"][t].cpu().view(torch.int16).numpy().view(np.uint16)
+        rl = vl["rows"][t].cpu().view(torch.int16).numpy().view(np.uint16)
+        for q in range(cl):
+            assert np.array_equal(rf[pb[q]:pb[q] + nr[q]], rl[pb[q]:pb[q] + nr[q]])
