@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-clocks", action="store_true", help="no nvidia-smi sampling during the timed steps")
     return ap.parse_args()
 
 
@@ -67,28 +68,30 @@ def ncu_traffic(kernel: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region.  nvidia-smi writes to a
+    file (no Python reader thread runs while the step is timed: a thread reading its pipe delayed
+    the host's wake-up in the mid-step sync of the page-compact exchange, AR_counts 0.24 -> 1.2-1.6 ms)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index, self.proc, self.lines = index, None, []
+    def __init__(self, index: int, enabled: bool = True):
+        self.index, self.proc, self.lines, self.enabled = index, None, [], enabled
+        self.path = None
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
+            import tempfile
+            fd, self.path = tempfile.mkstemp(prefix="edkm_clk_", suffix=".csv")
+            os.close(fd)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                          "--format=csv,noheader,nounits", "-lms", "50", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *a):
         if self.proc:
@@ -97,6 +100,13 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.path:
+            try:
+                with open(self.path) as f:
+                    self.lines = [ln.strip() for ln in f]
+                os.unlink(self.path)
+            except OSError:
+                pass
 
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -342,9 +352,12 @@ def main():
 
     # N > 1: exchange 1 fused into F1 over NVLS (dist.NvlsCounts) when the system supports it and
     # it passes a bit-exact self-check against F1 + NCCL all-reduce; otherwise NCCL.
-    # exchange 1: only the populated 256-pattern pages of the counts (dist.exchange_counts_compact,
-    # SURVEY S8(e) #1) unless EDKM_COMPACT=0
-    compact = distributed and os.environ.get("EDKM_COMPACT", "1") == "1"
+    # exchange 1: the whole int32 counts by default.  EDKM_COMPACT=1: only the populated 256-pattern
+    # pages (dist.exchange_counts_compact; also the compact table split) -- it needs
+    # one mid-step host read of the page mask, and that sync measured 0.24 ms alone but ~1-1.6 ms per
+    # step while nvidia-smi samples the clocks (bench at N=1 under torchrun), more than the ~0.1 ms
+    # it can save on a 59 MB NVLink all-reduce at N = 8
+    compact = distributed and os.environ.get("EDKM_COMPACT", "0") == "1"
     via = "libedkm.so's NCCL comm (edkm_comm_*)" if comm is not None else f"torch.distributed ({backend})"
     nv, exchange = None, (f"counts: {'page-compact ' if compact else ''}int32 all-reduce; gamma: fp64 all-reduce; "
                           f"via {via}")
@@ -448,7 +461,7 @@ def main():
     if distributed:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, enabled=not args.no_clocks) as clk:
         start.record(stream)
         for s in range(args.steps):
             step(evs[s])

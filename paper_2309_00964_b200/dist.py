@@ -62,10 +62,30 @@ def allreduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+_pinned = {}
+
+
 def union_pages(mask: torch.Tensor) -> torch.Tensor:
     """Global page ids t*256 + p of the pages set in the all-reduced [nt][256] mask, ascending (int32,
-    on the host: the mask's one device->host read).  Identical on every rank (the mask is)."""
-    return torch.nonzero(mask.reshape(-1).cpu()).reshape(-1).to(torch.int32)
+    on the host: the mask's one device->host read).  Identical on every rank (the mask is).
+
+    The read goes to a pinned buffer and the host spins on its event: a blocking stream sync that
+    waited out the rest of the previous step let the thread sleep, and its wake-up left the GPU idle
+    ~1.3 ms per step (bench at N=1 under torchrun: AR_counts 1.43 ms vs 0.25 ms in isolation)."""
+    if not mask.is_cuda:
+        return torch.nonzero(mask.reshape(-1)).reshape(-1).to(torch.int32)
+    n = mask.numel()
+    buf = _pinned.get("mask")
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _pinned["mask"] = buf
+    h = buf[:n]
+    h.copy_(mask.reshape(-1), non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    while not ev.query():
+        pass
+    return torch.nonzero(h).reshape(-1).to(torch.int32)
 
 
 def exchange_counts_compact(k, allreduce_sum_fn, allreduce_max_fn):
