@@ -65,6 +65,9 @@ def allreduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
 _pinned = {}
 
 
+_allreduce_max = allreduce_max  # (ShardedStep's parameter of the same name shadows it)
+
+
 def union_pages(mask: torch.Tensor) -> torch.Tensor:
     """Global page ids t*256 + p of the pages set in the all-reduced [nt][256] mask, ascending (int32,
     on the host: the mask's one device->host read).  Identical on every rank (the mask is).
@@ -153,7 +156,7 @@ class ShardedStep:
             self.allgather = allgather or (lambda t: comm.allgather_blocks(t))
         else:
             self.allreduce = allreduce or (lambda t: allreduce_sum(t, self.group))
-            self.allreduce_max = allreduce_max or (lambda t: globals()["allreduce_max"](t, self.group))
+            self.allreduce_max = allreduce_max or (lambda t: _allreduce_max(t, self.group))
             self.allgather = allgather or (lambda t: allgather_blocks(t, self.group))
         self.nvls = nvls
         self.shard_table = shard_table
