@@ -103,15 +103,13 @@ struct CSet {
   }
 };
 
-#ifndef EDKM_TF_F2D_INT
-#define EDKM_TF_F2D_INT 2
+// Rows per thread whose per-row products are summed in fp32 before one fp64 add (TF, TB): the
+// per-row arithmetic is fp32 (A itself carries ~2^-22 from ex2.approx), every sum over more rows
+// is fp64 (R7; tools/exp_tb_fp32.py: dC_0 within 1e-6, C_T within 6e-8 of the oracle).
+#ifndef EDKM_ROW_FLUSH
+#define EDKM_ROW_FLUSH 32
 #endif
-// exact fp32 -> fp64 of a normal or zero non-negative float (an ex2.approx.ftz result) by integer
-// ops: exponent rebias (+896 << 20 in the high word) and the mantissa split over both words
-__device__ __forceinline__ double f2d_pos(float a) {
-  const uint32_t f = __float_as_uint(a);
-  return __hiloint2double((int)(f ? (f >> 3) + 0x38000000u : 0u), (int)(f << 29));
-}
+constexpr int kRowFlush = EDKM_ROW_FLUSH;
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -147,21 +145,47 @@ __device__ __forceinline__ void attention_row(float vf, const CSet<K>& cs, float
   for (int j = 0; j < K; ++j) A[j] *= iz;
 }
 
-// The same without the fp32 normalisation: returns 1 / sum_j A[j] (TF applies it in fp64).
+// Sum of K floats in four interleaved chains, then pairwise: a fixed order (deterministic) with a
+// dependent chain of K/4 + 2 adds instead of K.
 template <int K>
-__device__ __forceinline__ float attention_row_raw(float vf, const CSet<K>& cs, float (&A)[K]) {
+__device__ __forceinline__ float sum4(const float (&a)[K]) {
+  if (K < 4) {
+    float z = a[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) z += a[j];
+    return z;
+  }
+  float z0 = a[0], z1 = a[1], z2 = a[2], z3 = a[3];
+#pragma unroll
+  for (int j = 4; j < K; j += 4) {
+    z0 += a[j];
+    z1 += a[j + 1];
+    z2 += a[j + 2];
+    z3 += a[j + 3];
+  }
+  return (z0 + z1) + (z2 + z3);
+}
+
+// 1/Z for Z >= 1 (the nearest centroid's term is ex2(0) = 1): MUFU rcp, ~1 ulp
+__device__ __forceinline__ float rcp_ge1(float z) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(z));
+  return y;
+}
+
+// The same without the normalisation: fills A with the unnormalised terms and returns 1 / sum_j A[j]
+// (the callers apply it to the sums that use A); `m` receives the nearest centroid's index.
+template <int K>
+__device__ __forceinline__ float attention_row_raw(float vf, const CSet<K>& cs, float (&A)[K], int& m) {
   const int jm = cs.nearest(vf);
+  m = jm;
   const float* dmr = cs.dms[jm];
   const float* phr = cs.ph[jm];
   const float* dplr = cs.dpl[jm];
   const float v2 = 2.0f * vf;
-  float Z = 0.0f;
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    A[j] = ex2(fmaf(-dmr[j], v2 - phr[j], dplr[j]));
-    Z += A[j];
-  }
-  return 1.0f / Z;
+  for (int j = 0; j < K; ++j) A[j] = ex2(fmaf(-dmr[j], v2 - phr[j], dplr[j]));
+  return rcp_ge1(sum4<K>(A));
 }
 
 // Warp sum of N doubles per lane (N a power of two <= 32) by a transposing butterfly: at the
@@ -196,14 +220,11 @@ __device__ __forceinline__ constexpr int log2i() { return N <= 1 ? 0 : 1 + log2i
 
 // Sum N doubles over the CTA then over the cluster; result in tot[0..N) of every CTA.
 // `part` is a [2][N] shared buffer used with alternating parity so one cluster
-// barrier per call suffices.
+// barrier per call suffices.  cluster_allreduce_red starts from per-warp sums already in
+// red[warp * N + i] (warp_flush); cluster_allreduce from one N-vector per thread.
 template <int N, int NW>
-__device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, double* part, double* tot, int parity,
-                                                  cg::cluster_group& cluster) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kShift = 5 - log2i<N>();
-  const double x = warp_transpose_sum<N>(v);
-  if ((lane & ((1 << kShift) - 1)) == 0) red[warp * N + (lane >> kShift)] = x;
+__device__ __forceinline__ void cluster_allreduce_red(const double* red, double* part, double* tot, int parity,
+                                                      cg::cluster_group& cluster) {
   __syncthreads();
   double* mine = part + parity * N;
   if (threadIdx.x < N) {
@@ -220,6 +241,38 @@ __device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, d
   __syncthreads();
 }
 
+template <int N, int NW>
+__device__ __forceinline__ void cluster_allreduce(double (&v)[N], double* red, double* part, double* tot, int parity,
+                                                  cg::cluster_group& cluster) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kShift = 5 - log2i<N>();
+  const double x = warp_transpose_sum<N>(v);
+  if ((lane & ((1 << kShift) - 1)) == 0) red[warp * N + (lane >> kShift)] = x;
+  cluster_allreduce_red<N, NW>(red, part, tot, parity, cluster);
+}
+
+// Warp-uniform: add the warp's fp32 per-lane partials af[0..N) (in fp64) to the warp's own
+// accumulator red_w[0..N) in shared memory (zeroed by warp_zero).  No fp64 accumulators stay
+// live in registers across the row loops.
+template <int N>
+__device__ __forceinline__ void warp_flush(float (&af)[N], double* red_w) {
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  constexpr int kShift = 5 - log2i<N>();
+  double v[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = (double)af[i];
+  const double x = warp_transpose_sum<N>(v);
+  if ((lane & ((1 << kShift) - 1)) == 0) red_w[lane >> kShift] += x;
+  __syncwarp();
+}
+template <int N>
+__device__ __forceinline__ void warp_zero(double* red_w) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < N; i += 32) red_w[i] = 0.0;
+  __syncwarp();
+}
+
 // Rows of one partition: patterns in rows[]; value (exact in fp32), count and the running psi
 // staged in shared memory for r < kStage, read from global memory beyond (U > kStage per CTA).
 struct RowStage {
@@ -233,6 +286,8 @@ struct RowStage {
   __device__ __forceinline__ double v(int r) const { return r < ns ? (double)sv[r] : decode16(rows[r], wdtype); }
   __device__ __forceinline__ double n(int r) const { return (double)(r < ns ? sn[r] : cnt[rows[r]]); }
   __device__ __forceinline__ double& psi(int r) const { return r < ns ? spsi[r] : gpsi[r]; }
+  __device__ __forceinline__ float vf(int r) const { return r < ns ? sv[r] : decode16f(rows[r], wdtype); }
+  __device__ __forceinline__ float nf(int r) const { return (float)(r < ns ? sn[r] : cnt[rows[r]]); }
   __device__ void stage() {
     for (int r = threadIdx.x; r < nr && r < ns; r += blockDim.x) {
       const uint32_t u = rows[r];
@@ -385,24 +440,34 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   for (int it = 0; it < P.max_iter; ++it) {
     cs.prepare(sC, P.inv_tau);
     __syncthreads();
-    double acc[2 * K];
+    double* red_w = red + warp * 2 * K;
+    warp_zero<2 * K>(red_w);
+    // warp-uniform blocks of at most kRowFlush rows per lane: S_j, M_j partials in fp32, then
+    // fp64 (R7); lane l of warp w takes rows w*32 + l + i*kFThreads
+    for (int rb = warp * 32; rb < nr; rb += kRowFlush * kFThreads) {
+      float af[2 * K];
 #pragma unroll
-    for (int j = 0; j < 2 * K; ++j) acc[j] = 0.0;
-    for (int r = tid; r < nr; r += kFThreads) {
-      const double v = R.v(r);
-      float A[K];
-      // 1/Z applied to the count in fp64 (n/Z, n v/Z) instead of to each A_j in fp32
-      const double nz = R.n(r) * (double)attention_row_raw<K>((float)v, cs, A), nvz = nz * v;
+      for (int j = 0; j < 2 * K; ++j) af[j] = 0.0f;
+      const int r1 = min(nr, rb + kRowFlush * kFThreads);
+      auto row = [&](float v, float n) {
+        float A[K];
+        int m;
+        // 1/Z applied to the count (n/Z, n v/Z) instead of to each A_j
+        const float nz = n * attention_row_raw<K>(v, cs, A, m), nvz = nz * v;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        // every EDKM_TF_F2D_INT-th conversion by integer ops (f2d_pos), the others by F2F: the
-        // XU pipe carries both the exponentials and F2F.F64.F32
-        const double a = (EDKM_TF_F2D_INT && j % EDKM_TF_F2D_INT == 0) ? f2d_pos(A[j]) : (double)A[j];
-        acc[j] = fma(a, nz, acc[j]);
-        acc[K + j] = fma(a, nvz, acc[K + j]);
+        for (int j = 0; j < K; ++j) {
+          af[j] = fmaf(A[j], nz, af[j]);
+          af[K + j] = fmaf(A[j], nvz, af[K + j]);
+        }
+      };
+      if (r1 <= R.ns) {  // staged rows (the usual case): shared memory only
+        for (int r = rb + lane; r < r1; r += kFThreads) row(R.sv[r], (float)R.sn[r]);
+      } else {
+        for (int r = rb + lane; r < r1; r += kFThreads) row(R.vf(r), R.nf(r));
       }
+      warp_flush<2 * K>(af, red_w);
     }
-    cluster_allreduce<2 * K, kFThreads / 32>(acc, red, part, tot, it & 1, cluster);
+    cluster_allreduce_red<2 * K, kFThreads / 32>(red, part, tot, it & 1, cluster);
     if (tid < K) {
       const double S = tot[tid], M = tot[K + tid];
       const double cn = (S != 0.0) ? M / S : sC[tid];
@@ -499,13 +564,85 @@ __global__ void __launch_bounds__(kFThreads, K <= 8 ? 4 : 2) tgamma_kernel(const
 }
 
 // ============================================================================ TB
-template <int K, int kBThreads, int kStageB>
-__global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
+// Per-iteration constants of the reverse loop in the forms one row needs, all derived in fp64 and
+// rounded once.  With m the row's nearest centroid (the one attention_row reduces against):
+//   gh'_j = gh_j - gh_m = (g1_j - g1_m) v - (g2_j - g2_m),  gh_j = g1_j v - g2_j = dL/dA_t[u][j],
+//   dz_l  = h1 (v - C_t[l]) = dzm + h1 (C_t[m] - C_t[l]),    dzm = h1 (v - C_t[m]) (float-float),
+// g1_j = G_j / S_j, g2_j = g1_j C_{t+1}[j], h1 = 2/tau.  The softmax Jacobian only sees gh up to a
+// constant, so gh' gives the same rr_l = A_l (gh_l - sum_j A_j gh_j) when sum_j A_j = 1 -- and when
+// it is not (fp32 normalisation) the constant gh_m no longer leaks in; gh'_m = 0 exactly and dzm is
+// accurate where v is near C_t[m], the row's largest attention (R7; tools/exp_tb_fp32.py).
+template <int K>
+struct BSet {
+  float g1[K];
+  float g1d[K][K], g2d[K][K], dh[K][K];
+  float h2hi[K], h2lo[K];
+  // every thread of the block calls it; the caller synchronises before and after
+  __device__ void prepare(const double* G, const double* cn, const double* S, const double* c, float h1f) {
+    const int t = threadIdx.x;
+    if (t < K * K) {
+      const int m = t / K, j = t % K;
+      const double ism = S[m] != 0.0 ? 1.0 / S[m] : 0.0, isj = S[j] != 0.0 ? 1.0 / S[j] : 0.0;
+      const double g1m = G[m] * ism, g1j = G[j] * isj;
+      g1d[m][j] = (float)(g1j - g1m);
+      g2d[m][j] = (float)(g1j * cn[j] - g1m * cn[m]);
+      dh[m][j] = (float)((double)h1f * (c[m] - c[j]));
+    }
+    if (t < K) {
+      const double is = S[t] != 0.0 ? 1.0 / S[t] : 0.0;
+      g1[t] = (float)(G[t] * is);
+      const double h = (double)h1f * c[t];
+      h2hi[t] = (float)h;
+      h2lo[t] = (float)(h - (double)h2hi[t]);
+    }
+  }
+};
+
+// One row of the reverse loop at iteration t, in fp32 (R7): adds n * q_l to af[l] (the row's
+// contribution to dL/dC_t[l]) and returns the row's psi increment (dL/dv through A_t and M_t).
+//   A = softmax attention (unnormalised here, 1/Z applied to the three sums that use it)
+//   rr_l = A_l (gh_l - sum_j A_j gh_j),  q_l = rr_l dz_l,  dpsi = sum_j A_j g1_j - sum_l q_l
+template <int K>
+__device__ __forceinline__ float tb_row(float v, float n, const CSet<K>& cs, const BSet<K>& bs, float h1f,
+                                        float (&af)[K]) {
+  float A[K];
+  int m;
+  const float iz = attention_row_raw<K>(v, cs, A, m);
+  const float* g1r = bs.g1d[m];
+  const float* g2r = bs.g2d[m];
+  const float* dhr = bs.dh[m];
+  float gh[K], p[K], d[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    gh[j] = fmaf(g1r[j], v, -g2r[j]);  // gh'_j (zero where S_t[j] = 0 and S_t[m] = 0)
+    p[j] = A[j] * gh[j];
+    d[j] = A[j] * bs.g1[j];            // direct path of v through M_t
+  }
+  const float s = sum4<K>(p) * iz;
+  const float dzm = fmaf(h1f, v, -bs.h2hi[m]) - bs.h2lo[m];
+  const float niz = n * iz;
+#pragma unroll
+  for (int l = 0; l < K; ++l) {
+    const float q = fmaf(-A[l], s, p[l]) * (dzm + dhr[l]);  // Z * rr_l * dz_l
+    p[l] = q;
+    af[l] = fmaf(niz, q, af[l]);
+  }
+  return iz * (sum4<K>(d) - sum4<K>(p));
+}
+
+// Reverse loop t = T-1..0: psi[u] and dC_0; then the (phi, psi) table.  The running psi is kept
+// in shared memory next to the staged rows (kPsiShared, 16 B per staged row: k = 16, two CTAs
+// per SM at 128 registers) or in global memory (8 B per staged row, L2-resident: k <= 8, four
+// CTAs per SM; CFG3 k = 8 TB 0.241 -> 0.217 ms, CFG4 k = 4 1.79 -> 1.43 ms in round 2).
+template <int K, int kStageB, int kMinBlocks, bool kPsiShared>
+__global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableArgs P) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
+  const int lane = tid & 31, warp = tid >> 5;
+  __shared__ double sG[K], sInvS[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
   __shared__ CSet<K> cs;
+  __shared__ BSet<K> bs;
   const double* sCt = cs.c;
   const TensorState* st = P.state + t;
   const int T = st->T, pcl = st->cl;
@@ -517,59 +654,54 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
   // heuristic in TF) that is the single partition `crank`, staged in shared memory
   const bool one = pcl == cl;
   const int pb0 = one ? st->pbase[crank] : 0;
-  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem + kStageB),
-             reinterpret_cast<int32_t*>(stage_mem + kStageB) + kStageB, stage_mem, psi + pb0,
+  double* vn_mem = kPsiShared ? stage_mem + kStageB : stage_mem;
+  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(vn_mem),
+             reinterpret_cast<int32_t*>(vn_mem) + kStageB, kPsiShared ? stage_mem : nullptr, psi + pb0,
              one ? st->nrows[crank] : 0, P.wdtype, kStageB};
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
   __syncthreads();
-  const double h1 = 2.0 * P.inv_tau;
+  const float h1f = (float)(2.0 * P.inv_tau);
   for (int it = T - 1; it >= 0; --it) {
     cs.prepare(ctraj + (int64_t)it * K, P.inv_tau);
+    bs.prepare(sG, ctraj + (int64_t)(it + 1) * K, straj + (int64_t)it * K, ctraj + (int64_t)it * K, h1f);
     if (tid < K) {
-      // per-iteration constants: gh_j = g1_j v - g2_j, dz_l = h1 v - h2_l
-      const double cn = ctraj[(int64_t)(it + 1) * K + tid];
       const double S = straj[(int64_t)it * K + tid];
-      const double is = S != 0.0 ? 1.0 / S : 0.0;
-      sInvS[tid] = is;
-      sG1[tid] = sG[tid] * is;
-      sG2[tid] = sG[tid] * cn * is;
-      sH2[tid] = h1 * ctraj[(int64_t)it * K + tid];
+      sInvS[tid] = S != 0.0 ? 1.0 / S : 0.0;
     }
     __syncthreads();
-    double acc[K];
-#pragma unroll
-    for (int l = 0; l < K; ++l) acc[l] = 0.0;
+    double* red_w = red + warp * K;
+    warp_zero<K>(red_w);
     for (int p = crank; p < pcl; p += cl) {
       const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
       double* gpsi = psi + st->pbase[p];
       const int nr = one ? R.nr : st->nrows[p];
-      for (int r = tid; r < nr; r += kBThreads) {
-        const double v = one ? R.v(r) : decode16(rows[r], P.wdtype);
-        const double n = one ? R.n(r) : (double)cnt[rows[r]];
-        float Af[K];
-        attention_row<K>((float)v, cs, Af);
-        double A[K], gh[K];
-        double s = 0.0, dpsi = 0.0;
+      // warp-uniform blocks of at most kRowFlush rows per lane: the n-weighted sums in fp32,
+      // then fp64 (R7); lane l of warp w takes rows w*32 + l + i*kBThreads
+      for (int rb = warp * 32; rb < nr; rb += kRowFlush * kBThreads) {
+        float af[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          A[j] = (double)Af[j];
-          gh[j] = fma(sG1[j], v, -sG2[j]);           // dL/dA_t[u][j] (zero where S_t[j] = 0)
-          s = fma(A[j], gh[j], s);
-          dpsi = fma(A[j], sG1[j], dpsi);             // direct path of v through M_t
+        for (int l = 0; l < K; ++l) af[l] = 0.0f;
+        const int r1 = min(nr, rb + kRowFlush * kBThreads);
+        if (one && r1 <= R.ns) {  // staged rows (the usual case)
+          for (int r = rb + lane; r < r1; r += kBThreads) {
+            double& ps = kPsiShared ? R.spsi[r] : gpsi[r];
+            const double ps_old = it == T - 1 ? 0.0 : ps;  // issued before the row's arithmetic
+            ps = ps_old + (double)tb_row<K>(R.sv[r], (float)R.sn[r], cs, bs, h1f, af);
+          }
+        } else {
+          for (int r = rb + lane; r < r1; r += kBThreads) {
+            const float v = one ? R.vf(r) : decode16f(rows[r], P.wdtype);
+            const float n = one ? R.nf(r) : (float)cnt[rows[r]];
+            double& ps = (kPsiShared && one) ? R.psi(r) : gpsi[r];
+            const double ps_old = it == T - 1 ? 0.0 : ps;
+            ps = ps_old + (double)tb_row<K>(v, n, cs, bs, h1f, af);
+          }
         }
-#pragma unroll
-        for (int l = 0; l < K; ++l) {
-          const double rr = A[l] * (gh[l] - s);      // softmax Jacobian applied to gh
-          const double q = rr * fma(h1, v, -sH2[l]);  // rr * dz_l, dz_l = 2 (v - C_t[l]) / tau
-          dpsi -= q;
-          acc[l] = fma(n, q, acc[l]);
-        }
-        double& ps = one ? R.psi(r) : gpsi[r];
-        ps = (it == T - 1 ? 0.0 : ps) + dpsi;
+        warp_flush<K>(af, red_w);
       }
     }
-    cluster_allreduce<K, kBThreads / 32>(acc, red, part, tot, it & 1, cluster);
+    cluster_allreduce_red<K, kBThreads / 32>(red, part, tot, it & 1, cluster);
     if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
     __syncthreads();
   }
@@ -593,193 +725,11 @@ __global__ void __launch_bounds__(kBThreads) tb_kernel(const TableArgs P) {
       double var = 0.0;
 #pragma unroll
       for (int l = 0; l < K; ++l) var += (double)Af[l] * (sCt[l] - wt) * (sCt[l] - wt);
-      const double ps = T > 0 ? (one ? R.psi(r) : gpsi[r]) : 0.0;
+      const double ps = T > 0 ? ((kPsiShared && one) ? R.psi(r) : gpsi[r]) : 0.0;
       pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
     }
     // NaN/Inf patterns (dW = NaN, R10) and absent patterns (no weight uses them): NaN.
     // 16 patterns per thread per step (vector loads of the counts).
-    const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
-    for (int u0 = st->pbase[p] + tid * 16; u0 < st->pbase[p + 1]; u0 += kBThreads * 16) {
-      const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
-      int c[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int4 x = __ldg(c4 + q);
-        c[4 * q] = x.x;
-        c[4 * q + 1] = x.y;
-        c[4 * q + 2] = x.z;
-        c[4 * q + 3] = x.w;
-      }
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (!pattern_finite(u0 + e, P.wdtype) || c[e] == 0) pp[u0 + e] = nan2;
-    }
-  }
-  cluster.sync();
-}
-
-// ============================================================================ TB, split rows
-// The same reverse loop with each row's K centroids split over H adjacent lanes (KH = K/H each;
-// H = 1 in the build: see launch_tb_k) and the running psi kept in global memory (L2-resident:
-// 8 B per row) instead of shared memory.
-// TB<16> in one lane per row needs 128 registers (A, gh and the K accumulators in fp64) and
-// 100 KiB of staged rows: 16 warps per SM, and its per-row fp64 chains (s = sum_j A_j gh_j and
-// psi, 16 and 32 dependent adds) leave the FP64 pipe ~60% idle (ncu r01c).  Split over H = 2 lanes
-// every chain halves, a lane holds K/2 of the per-centroid state, and with v, n alone staged
-// (8 B per row) four CTAs fit per SM.  Sums over the row's centroids are combined by one xor
-// shuffle; the k-vector reduction over rows stays in fixed order (deterministic, rank-identical).
-template <int N, int NW, int H>
-__device__ __forceinline__ void cluster_allreduce_h(double (&v)[N / H], double* red, double* part, double* tot,
-                                                    int parity, cg::cluster_group& cluster) {
-  constexpr int NH = N / H;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane % H;
-  if (H == 1) {
-    constexpr int kShift = 5 - log2i<N>();
-    const double x = warp_transpose_sum<NH>(v);
-    if ((lane & ((1 << kShift) - 1)) == 0) red[warp * N + (lane >> kShift)] = x;
-  } else {
-#pragma unroll
-    for (int n = 0; n < NH; ++n) {
-      double x = v[n];
-#pragma unroll
-      for (int o = 16; o >= H; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane < H) red[warp * N + sub * NH + n] = x;
-    }
-  }
-  __syncthreads();
-  double* mine = part + parity * N;
-  if (threadIdx.x < N) {
-    double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += red[w * N + threadIdx.x];
-    mine[threadIdx.x] = s;
-  }
-  cluster.sync();
-  if (threadIdx.x < N) {
-    double s = 0.0;
-    for (unsigned r = 0; r < cluster.num_blocks(); ++r) s += cluster.map_shared_rank(mine, r)[threadIdx.x];
-    tot[threadIdx.x] = s;
-  }
-  __syncthreads();
-}
-
-template <int K, int H, int kStageB, int kMinBlocks>
-__global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_split_kernel(const TableArgs P) {
-  constexpr int KH = K / H;
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(16) double stage_mem[];
-  const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
-  const int sub = (tid & 31) % H, slot = tid / H, nslots = kBThreads / H;
-  __shared__ double sG[K], sInvS[K], sG1[K], sG2[K], sH2[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
-  __shared__ CSet<K> cs;
-  const double* sCt = cs.c;
-  const TensorState* st = P.state + t;
-  const int T = st->T, pcl = st->cl;
-  const int32_t* cnt = P.counts + (int64_t)t * kPatterns;
-  const double* ctraj = P.ctraj + (int64_t)t * (P.max_iter + 1) * K;
-  const double* straj = P.straj + (int64_t)t * (P.max_iter > 0 ? P.max_iter : 1) * K;
-  double* psi_t = P.psi + (int64_t)t * kPatterns;
-  // this CTA owns partitions p = crank, crank + cl, ...; with pcl == cl (always, same heuristic
-  // in TF) that is the single partition `crank`, whose value and count are staged
-  const bool one = pcl == cl;
-  const int pb0 = one ? st->pbase[crank] : 0;
-  RowStage R{P.rows + (int64_t)t * kPatterns + pb0, cnt, reinterpret_cast<float*>(stage_mem),
-             reinterpret_cast<int32_t*>(stage_mem) + kStageB, nullptr, nullptr, one ? st->nrows[crank] : 0,
-             P.wdtype, kStageB};
-  if (one) R.stage();
-  if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
-  __syncthreads();
-  const double h1 = 2.0 * P.inv_tau;
-  for (int it = T - 1; it >= 0; --it) {
-    cs.prepare(ctraj + (int64_t)it * K, P.inv_tau);
-    if (tid < K) {
-      const double cn = ctraj[(int64_t)(it + 1) * K + tid];
-      const double S = straj[(int64_t)it * K + tid];
-      const double is = S != 0.0 ? 1.0 / S : 0.0;
-      sInvS[tid] = is;
-      sG1[tid] = sG[tid] * is;
-      sG2[tid] = sG[tid] * cn * is;
-      sH2[tid] = h1 * ctraj[(int64_t)it * K + tid];
-    }
-    __syncthreads();
-    double acc[KH];
-#pragma unroll
-    for (int l = 0; l < KH; ++l) acc[l] = 0.0;
-    for (int p = crank; p < pcl; p += cl) {
-      const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
-      double* gpsi = psi_t + st->pbase[p];
-      const int nr = one ? R.nr : st->nrows[p];
-      // every lane of a row group runs the same trip count (the shuffles need the whole warp)
-      for (int r0 = slot - slot % (32 / H); r0 < nr; r0 += nslots) {
-        const int r = r0 + slot % (32 / H);
-        const bool live = r < nr && r0 < nr;
-        const int rr_ = live ? r : 0;
-        const double v = (nr > 0) ? (one ? R.v(rr_) : decode16(rows[rr_], P.wdtype)) : 0.0;
-        const double n = live ? (one ? R.n(rr_) : (double)cnt[rows[rr_]]) : 0.0;
-        double ps_old = 0.0;
-        if (live && sub == 0 && it != T - 1) ps_old = gpsi[r];  // issued early, used at the end
-        // attention of the row to this lane's KH centroids, normalised over all K (fp32, R7)
-        const float vf = (float)v;
-        const int jm = cs.nearest(vf);
-        const float v2 = 2.0f * vf;
-        float Af[KH];
-        float Z = 0.0f;
-#pragma unroll
-        for (int jj = 0; jj < KH; ++jj) {
-          const int j = sub * KH + jj;
-          Af[jj] = ex2(fmaf(-cs.dms[jm][j], v2 - cs.ph[jm][j], cs.dpl[jm][j]));
-          Z += Af[jj];
-        }
-        if (H == 2) Z += __shfl_xor_sync(0xffffffffu, Z, 1);
-        const float iz = 1.0f / Z;
-        double A[KH], gh[KH];
-        double s = 0.0, dpsi = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < KH; ++jj) {
-          const int j = sub * KH + jj;
-          A[jj] = (double)(Af[jj] * iz);
-          gh[jj] = fma(sG1[j], v, -sG2[j]);  // dL/dA_t[u][j] (zero where S_t[j] = 0)
-          s = fma(A[jj], gh[jj], s);
-          dpsi = fma(A[jj], sG1[j], dpsi);   // direct path of v through M_t
-        }
-        if (H == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
-#pragma unroll
-        for (int jj = 0; jj < KH; ++jj) {
-          const int l = sub * KH + jj;
-          const double rr = A[jj] * (gh[jj] - s);     // softmax Jacobian applied to gh
-          const double q = rr * fma(h1, v, -sH2[l]);  // rr * dz_l, dz_l = 2 (v - C_t[l]) / tau
-          dpsi -= q;
-          acc[jj] = fma(n, q, acc[jj]);
-        }
-        if (H == 2) dpsi += __shfl_xor_sync(0xffffffffu, dpsi, 1);
-        if (live && sub == 0) gpsi[r] = ps_old + dpsi;
-      }
-    }
-    cluster_allreduce_h<K, kBThreads / 32, H>(acc, red, part, tot, it & 1, cluster);
-    if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
-    __syncthreads();
-  }
-  if (crank == 0 && tid < K) P.dC0[(int64_t)t * K + tid] = (float)sG[tid];
-  // (phi, psi) table: phi[u] = (2/tau) sum_l A_T[u,l] (C_T[l] - W~_u)^2 (one row per thread)
-  cs.prepare(ctraj + (int64_t)T * K, P.inv_tau);
-  __syncthreads();
-  float2* pp = P.phipsi + (int64_t)t * kPatterns;
-  for (int p = crank; p < pcl; p += cl) {
-    const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
-    const double* gpsi = psi_t + st->pbase[p];
-    const int nr = one ? R.nr : st->nrows[p];
-    for (int r = tid; r < nr; r += kBThreads) {
-      const uint32_t u = rows[r];
-      const double v = one ? R.v(r) : decode16(u, P.wdtype);
-      float Af[K];
-      attention_row<K>((float)v, cs, Af);
-      double wt = 0.0;
-#pragma unroll
-      for (int l = 0; l < K; ++l) wt = fma((double)Af[l], sCt[l], wt);
-      double var = 0.0;
-#pragma unroll
-      for (int l = 0; l < K; ++l) var += (double)Af[l] * (sCt[l] - wt) * (sCt[l] - wt);
-      pp[u] = make_float2((float)(2.0 * P.inv_tau * var), T > 0 ? (float)gpsi[r] : 0.0f);
-    }
     const float2 nan2 = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
     for (int u0 = st->pbase[p] + tid * 16; u0 < st->pbase[p + 1]; u0 += kBThreads * 16) {
       const int4* c4 = reinterpret_cast<const int4*>(cnt + u0);
@@ -807,10 +757,16 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_split_kernel(const T
 // tensor) more, smaller partitions measured slower for 226 tensors (cl = 5: TF 0.15 -> 0.26 ms,
 // TB 0.27 -> 0.47 ms on CFG3).  fp16 tensors have ~5x the rows (U ~ 24K): with cl = 4 and TB's
 // two-CTAs-per-SM shape, CFG4 (k = 16) TB 4.06 -> 3.76 ms, k = 4 TB 1.93 -> 1.79 ms.
+#ifndef EDKM_CL_FP16
+#define EDKM_CL_FP16 4
+#endif
+#ifndef EDKM_CL_BF16
+#define EDKM_CL_BF16 2
+#endif
 int table_cluster_size(int nt, int wdtype) {
   if (nt <= 18) return 8;
   if (nt <= 37) return 4;
-  return wdtype == kFP16 ? 4 : 2;
+  return wdtype == kFP16 ? EDKM_CL_FP16 : EDKM_CL_BF16;
 }
 
 template <class Fn>
@@ -846,12 +802,15 @@ static cudaError_t launch_table(const TableArgs& P, cudaStream_t s, Fn fn, size_
     }                                                            \
   }
 
+#ifndef EDKM_TF16_MB
+#define EDKM_TF16_MB 3
+#endif
 template <int K>
 static cudaError_t launch_tf_k(const TableArgs& P, cudaStream_t s) {
   if (P.wdtype == kBF16)
     return launch_table(P, s, tf_kernel<K, kStageFS, 4>, (size_t)kStageFS * 8, kFThreads);
   // fp16: ~6K rows per CTA at cl = 4; four CTAs per SM where k <= 8 fits 64 registers
-  return launch_table(P, s, tf_kernel<K, kStageFL, (K <= 8 ? 4 : 2)>, (size_t)kStageFL * 8, kFThreads);
+  return launch_table(P, s, tf_kernel<K, kStageFL, (K <= 8 ? 4 : EDKM_TF16_MB)>, (size_t)kStageFL * 8, kFThreads);
 }
 
 cudaError_t launch_tf(const TableArgs& P, cudaStream_t s) {
@@ -864,27 +823,24 @@ cudaError_t launch_tf(const TableArgs& P, cudaStream_t s) {
   }
 }
 EDKM_TABLE_LAUNCH(launch_tgamma, tgamma_kernel, 0, kFThreads)
-// TB variant per k (measured, S4): k <= 8 run tb_split_kernel with one lane per row and
-// psi in global memory, four CTAs per SM (CFG3 k = 8 TB 0.241 -> 0.217 ms, CFG4 k = 4 1.79 ->
-// 1.43 ms); k = 16 keeps tb_kernel (128 registers, psi staged): split over two lanes it measured
-// 3.67 -> 5.2-5.6 ms (duplicated nearest-centroid search, runtime centroid offsets, shuffles).
-#ifndef EDKM_TB_SPLIT_MAXK
-#define EDKM_TB_SPLIT_MAXK 8
-#endif
-#ifndef EDKM_TB_H2_MINK
-#define EDKM_TB_H2_MINK 32
+// TB variant per k (measured, S4): k <= 8 keep psi in global memory and run four CTAs
+// per SM; k = 16 (128 registers) keeps psi staged in shared memory at two CTAs per SM.
+#ifndef EDKM_TB16_MB
+#define EDKM_TB16_MB 2
 #endif
 template <int K>
 static cudaError_t launch_tb_k(const TableArgs& P, cudaStream_t s) {
-  if (K <= EDKM_TB_SPLIT_MAXK) {
-    constexpr int H = K >= EDKM_TB_H2_MINK ? 2 : 1, MB = 4;
+  if constexpr (K <= 8) {
     if (P.wdtype == kBF16)
-      return launch_table(P, s, tb_split_kernel<K, H, kStageB16, MB>, (size_t)kStageB16 * 8, kBThreads);
-    return launch_table(P, s, tb_split_kernel<K, H, kStageB32, MB>, (size_t)kStageB32 * 8, kBThreads);
+      return launch_table(P, s, tb_kernel<K, kStageB16, 4, false>, (size_t)kStageB16 * 8, kBThreads);
+    return launch_table(P, s, tb_kernel<K, kStageB32, 4, false>, (size_t)kStageB32 * 8, kBThreads);
+  } else {
+    constexpr int MB = EDKM_TB16_MB;
+    constexpr bool PS = MB <= 2;  // psi staged next to the rows only at two CTAs per SM
+    if (P.wdtype == kBF16)
+      return launch_table(P, s, tb_kernel<K, kStageB16, MB, PS>, (size_t)kStageB16 * (PS ? 16 : 8), kBThreads);
+    return launch_table(P, s, tb_kernel<K, kStageB32, MB, PS>, (size_t)kStageB32 * (PS ? 16 : 8), kBThreads);
   }
-  if (P.wdtype == kBF16)
-    return launch_table(P, s, tb_kernel<K, kBThreads, kStageB16>, (size_t)kStageB16 * 16, kBThreads);
-  return launch_table(P, s, tb_kernel<K, kBThreads, kStageB32>, (size_t)kStageB32 * 16, kBThreads);
 }
 
 cudaError_t launch_tb(const TableArgs& P, cudaStream_t s) {
