@@ -586,6 +586,25 @@ def main():
             "frac_of_spec_8tbs": achieved / 8000.0,
             "step_frac": (16 * n_local / (ms_max / 1e3) / 1e9) / peak,
             "step_frac_of_spec_8tbs": (16 * n_local / (ms_max / 1e3) / 1e9) / 8000.0}
+    # ---- roofline of the table phase (TF + TGAMMA + TB): one ex2 per attention entry is the method's
+    # irreducible transcendental work (U rows x k centroids per forward iteration, per reverse
+    # iteration, and once each for the W~ table, gamma_T and the (phi, psi) table), counted from the
+    # populated rows and the iterations each tensor ran; the peak is the MUFU ex2 rate measured on a
+    # B200 (tools/ubench_mufu.cu, profiles/ubench_mufu_r02.txt: 15.97 ex2/clk/SM) at this run's
+    # median SM clock.  The per-row arithmetic is fp32 FFMA/FADD around it (DESIGN S4), so the
+    # kernels are issue-bound below this figure.
+    tb0, tb1 = (t0, t1) if shard else (0, plan.nt)
+    _, iters = E.read_status(plan.saved, plan.nt, p)
+    rows_t = (plan.counts[tb0:tb1] != 0).sum(dim=1).tolist()
+    ex2 = sum(u * wl.k * (2 * it + 3) for u, it in zip(rows_t, iters[tb0:tb1]))
+    t_table = phase["TF"] + phase["TGAMMA"] + phase["TB"]
+    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+    ex2_peak = 15.97 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
+    table_roof = {"bound": "xu", "op": "ex2.approx.ftz.f32 (one per attention entry)", "kernels": "TF+TGAMMA+TB",
+                  "rows": int(sum(rows_t)), "ex2_per_step": int(ex2), "ms": t_table,
+                  "achieved": ex2 / (t_table / 1e3), "peak": ex2_peak, "unit": "ex2/s",
+                  "frac": ex2 / (t_table / 1e3) / ex2_peak,
+                  "peak_source": f"measured 15.97 ex2/clk/SM (tools/ubench_mufu.cu) x SMs x {sm_mhz:.0f} MHz"}
     out = {
         "metric": METRIC, "value": n_total / (ms_max / 1e3), "unit": "weights/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -598,10 +617,11 @@ def main():
                    "table_phase": ("split by tensor block + " + ("page-compact exchange" if compact and nv is None
                                                                   else "all-gather") if shard
                                    else "replicated on every rank"),
-                   "arith": f"{w16} I/O; exact integer F1/B1 sums, fp32 B2 FMA; fp64 table phase",
+                   "arith": f"{w16} I/O; exact integer F1/B1 sums, fp32 B2 FMA; table phase: fp32 per row "
+                            "(ex2.approx), fp64 sums over rows, centroids and trajectories",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
         "phases_ms": phase, "gpu_launches": launches_per_step * args.steps, "rank_identical_C_dC0": rank_identical,
-        "clocks": clk.summary(), "roofline": roof, "e2e": e2e, "cuda_graph": graph,
+        "clocks": clk.summary(), "roofline": roof, "table_roofline": table_roof, "e2e": e2e, "cuda_graph": graph,
     }
     if not args.no_cpu_baseline:  # rank 0 (at N > 1 too): the oracle on the host cores + the step's parity
         def gpu_result(t):

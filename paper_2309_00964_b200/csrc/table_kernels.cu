@@ -166,6 +166,26 @@ __device__ __forceinline__ float sum4(const float (&a)[K]) {
   return (z0 + z1) + (z2 + z3);
 }
 
+// sum_j a_j b_j in four interleaved FFMA chains, then pairwise (fixed order, as sum4)
+template <int K>
+__device__ __forceinline__ float dot4(const float (&a)[K], const float* b) {
+  if (K < 4) {
+    float z = a[0] * b[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) z = fmaf(a[j], b[j], z);
+    return z;
+  }
+  float z0 = a[0] * b[0], z1 = a[1] * b[1], z2 = a[2] * b[2], z3 = a[3] * b[3];
+#pragma unroll
+  for (int j = 4; j < K; j += 4) {
+    z0 = fmaf(a[j], b[j], z0);
+    z1 = fmaf(a[j + 1], b[j + 1], z1);
+    z2 = fmaf(a[j + 2], b[j + 2], z2);
+    z3 = fmaf(a[j + 3], b[j + 3], z3);
+  }
+  return (z0 + z1) + (z2 + z3);
+}
+
 // 1/Z for Z >= 1 (the nearest centroid's term is ex2(0) = 1): MUFU rcp, ~1 ulp
 __device__ __forceinline__ float rcp_ge1(float z) {
   float y;
@@ -305,8 +325,8 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  __shared__ double sC[K], sCn[K], sCf[K], sDelta[K];
-  __shared__ double red[(kFThreads / 32) * 2 * K], part[2 * 2 * K], tot[2 * K];
+  __shared__ double sCb[2][K], sCf[K], sDelta[K];  // C_t / C_{t+1}, alternating by iteration parity
+  __shared__ double red[(kFThreads / 32) * 2 * K], part[2 * 2 * K];
   __shared__ CSet<K> cs;
   __shared__ int s_scan[(kFThreads / 32)];
   __shared__ long long s_nf[(kFThreads / 32)];
@@ -432,14 +452,19 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   double* ctraj = P.ctraj + (int64_t)t * stride_c;
   double* straj = P.straj + (int64_t)t * stride_s;
   if (tid < K) {
-    sC[tid] = (double)P.C0[(int64_t)t * K + tid];
-    if (crank == 0) ctraj[tid] = sC[tid];
+    sCb[0][tid] = (double)P.C0[(int64_t)t * K + tid];
+    if (crank == 0) ctraj[tid] = sCb[0][tid];
   }
   __syncthreads();
   int T = P.max_iter;
+  if (P.max_iter > 0) cs.prepare(sCb[0], P.inv_tau);
+  __syncthreads();
+  // Per iteration: the row loop, one CTA barrier + one cluster barrier for the sums, the centroid
+  // update by K threads straight from the cluster's partial sums, one barrier, the next
+  // iteration's tables, one barrier (round 2: five CTA barriers before).
   for (int it = 0; it < P.max_iter; ++it) {
-    cs.prepare(sC, P.inv_tau);
-    __syncthreads();
+    const double* sC = sCb[it & 1];
+    double* sCn = sCb[(it + 1) & 1];
     double* red_w = red + warp * 2 * K;
     warp_zero<2 * K>(red_w);
     // warp-uniform blocks of at most kRowFlush rows per lane: S_j, M_j partials in fp32, then
@@ -467,9 +492,22 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
       }
       warp_flush<2 * K>(af, red_w);
     }
-    cluster_allreduce_red<2 * K, kFThreads / 32>(red, part, tot, it & 1, cluster);
+    // the CTA's sums (warp order), then the cluster's (CTA order) read by the K updating threads
+    __syncthreads();
+    double* mine = part + (it & 1) * 2 * K;
+    if (tid < 2 * K) {
+      double x = 0.0;
+      for (int w = 0; w < kFThreads / 32; ++w) x += red[w * 2 * K + tid];
+      mine[tid] = x;
+    }
+    cluster.sync();
     if (tid < K) {
-      const double S = tot[tid], M = tot[K + tid];
+      double S = 0.0, M = 0.0;
+      for (unsigned r = 0; r < cluster.num_blocks(); ++r) {
+        const double* q = cluster.map_shared_rank(mine, r);
+        S += q[tid];
+        M += q[K + tid];
+      }
       const double cn = (S != 0.0) ? M / S : sC[tid];
       sCn[tid] = cn;
       sDelta[tid] = fabs(cn - sC[tid]);
@@ -482,13 +520,14 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
     double dmax = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) dmax = fmax(dmax, sDelta[j]);
-    if (tid < K) sC[tid] = sCn[tid];
-    __syncthreads();
     if (P.eps > 0.0 && dmax <= P.eps) {  // identical on every CTA of the cluster
       T = it + 1;
       break;
     }
+    if (it + 1 < P.max_iter) cs.prepare(sCn, P.inv_tau);  // sDelta is rewritten only after the next barrier
+    __syncthreads();
   }
+  const double* sC = sCb[T & 1];
   if (crank == 0 && tid == 0) st->T = T;
   if (tid < K) {
     const float cf = (float)sC[tid];
@@ -541,21 +580,32 @@ __global__ void __launch_bounds__(kFThreads, K <= 8 ? 4 : 2) tgamma_kernel(const
   for (int p = crank; p < pcl; p += cl) {
     const uint16_t* rows = P.rows + (int64_t)t * kPatterns + st->pbase[p];
     const int nr = st->nrows[p];
-    for (int r = tid; r < nr; r += kFThreads) {
-      const uint32_t u = rows[r];
-      const double B = Bt[u];
-      if (B == 0.0) continue;
-      const double v = decode16(u, P.wdtype);
-      float Af[K];
-      attention_row<K>((float)v, cs, Af);
-      double A[K], wt = 0.0;
+    // four rows per thread per step: their pattern and bucket loads are issued together (the
+    // kernel is bound by these dependent global loads otherwise)
+    for (int r0 = tid; r0 < nr; r0 += 4 * kFThreads) {
+      uint32_t uq[4];
+      double Bq[4];
 #pragma unroll
-      for (int l = 0; l < K; ++l) {
-        A[l] = (double)Af[l];
-        wt = fma(A[l], sC[l], wt);
+      for (int q = 0; q < 4; ++q) uq[q] = r0 + q * kFThreads < nr ? (uint32_t)rows[r0 + q * kFThreads] : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Bq[q] = r0 + q * kFThreads < nr ? Bt[uq[q]] : 0.0;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t u = uq[q];
+        const double B = Bq[q];
+        if (B == 0.0) continue;
+        const double v = decode16(u, P.wdtype);
+        float Af[K];
+        attention_row<K>((float)v, cs, Af);
+        double A[K], wt = 0.0;
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+          A[l] = (double)Af[l];
+          wt = fma(A[l], sC[l], wt);
+        }
+#pragma unroll
+        for (int l = 0; l < K; ++l) acc[l] += B * A[l] * (1.0 + (sC[l] - wt) * 2.0 * (v - sC[l]) * P.inv_tau);
       }
-#pragma unroll
-      for (int l = 0; l < K; ++l) acc[l] += B * A[l] * (1.0 + (sC[l] - wt) * 2.0 * (v - sC[l]) * P.inv_tau);
     }
   }
   cluster_allreduce<K, kFThreads / 32>(acc, red, part, tot, 0, cluster);
@@ -611,13 +661,13 @@ __device__ __forceinline__ float tb_row(float v, float n, const CSet<K>& cs, con
   const float* g1r = bs.g1d[m];
   const float* g2r = bs.g2d[m];
   const float* dhr = bs.dh[m];
-  float gh[K], p[K], d[K];
+  float gh[K], p[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     gh[j] = fmaf(g1r[j], v, -g2r[j]);  // gh'_j (zero where S_t[j] = 0 and S_t[m] = 0)
     p[j] = A[j] * gh[j];
-    d[j] = A[j] * bs.g1[j];            // direct path of v through M_t
   }
+  const float dsum = dot4<K>(A, bs.g1);  // sum_j A_j g1_j: the direct path of v through M_t
   const float s = sum4<K>(p) * iz;
   const float dzm = fmaf(h1f, v, -bs.h2hi[m]) - bs.h2lo[m];
   const float niz = n * iz;
@@ -627,7 +677,7 @@ __device__ __forceinline__ float tb_row(float v, float n, const CSet<K>& cs, con
     p[l] = q;
     af[l] = fmaf(niz, q, af[l]);
   }
-  return iz * (sum4<K>(d) - sum4<K>(p));
+  return iz * (dsum - sum4<K>(p));
 }
 
 // Reverse loop t = T-1..0: psi[u] and dC_0; then the (phi, psi) table.  The running psi is kept
@@ -660,13 +710,30 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
              one ? st->nrows[crank] : 0, P.wdtype, kStageB};
   if (one) R.stage();
   if (tid < K) sG[tid] = P.gamma[(int64_t)t * K + tid];
+  // the iteration's C_t, C_{t+1} and S_t, copied to shared memory one iteration ahead (cp.async,
+  // no registers held across the row loop): the per-iteration tables are then built from shared
+  // memory instead of from dependent L2 loads (ncu r02: 8% of TB<16>'s stall samples)
+  __shared__ __align__(16) double sTr[2][3 * K];
+  auto fetch = [&](int it, int buf) {
+    if (tid < 3 * K) {
+      const double* src = tid < K ? ctraj + (int64_t)it * K + tid
+                                  : tid < 2 * K ? ctraj + (int64_t)(it + 1) * K + (tid - K) : straj + (int64_t)it * K + (tid - 2 * K);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(&sTr[buf][tid])), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (T > 0) fetch(T - 1, 0);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   const float h1f = (float)(2.0 * P.inv_tau);
   for (int it = T - 1; it >= 0; --it) {
-    cs.prepare(ctraj + (int64_t)it * K, P.inv_tau);
-    bs.prepare(sG, ctraj + (int64_t)(it + 1) * K, straj + (int64_t)it * K, ctraj + (int64_t)it * K, h1f);
+    const int buf = (T - 1 - it) & 1;
+    if (it > 0) fetch(it - 1, buf ^ 1);  // the other buffer: last read by the previous iteration's tables
+    const double* tr = sTr[buf];
+    cs.prepare(tr, P.inv_tau);
+    bs.prepare(sG, tr + K, tr + 2 * K, tr, h1f);
     if (tid < K) {
-      const double S = straj[(int64_t)it * K + tid];
+      const double S = tr[2 * K + tid];
       sInvS[tid] = S != 0.0 ? 1.0 / S : 0.0;
     }
     __syncthreads();
@@ -703,6 +770,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
     }
     cluster_allreduce_red<K, kBThreads / 32>(red, part, tot, it & 1, cluster);
     if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the next iteration's trajectories
     __syncthreads();
   }
   if (crank == 0 && tid < K) P.dC0[(int64_t)t * K + tid] = (float)sG[tid];

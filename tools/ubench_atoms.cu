@@ -1,0 +1,235 @@
+// Microbenchmark: F1's shared-array histogram loop (256-bit streaming loads, one red.shared.add.u32
+// per 16-bit pattern into 57344 u32 counters) on different pattern laws -- the question for a fp16
+// F1 (DESIGN S9): is the fp16 path's shared-atomic rate set by the bank law of fp16 N(0, 0.02^2)
+// patterns, and does a bank-scrambled counter address, or a G-lane-shared copy layout, change it?
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_atoms tools/ubench_atoms.cu
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdint>
+
+constexpr int kWords = 57344;  // 224 KiB
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
+}
+
+// law 0: fp16 N(0, 0.02^2); 1: bf16 N(0, 0.02^2); 2: uniform in [0, 0xE000)
+__global__ void gen(uint16_t* w, size_t n, int law) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t a = hash32((uint32_t)i * 2u + 17u), b = hash32((uint32_t)i * 2u + 1u + 99u);
+    const float u1 = (a + 1.0f) * 2.3283064e-10f, u2 = b * 2.3283064e-10f;
+    const float z = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2) * 0.02f;
+    uint16_t p;
+    if (law == 0) {
+      const __half h = __float2half_rn(z);
+      p = *reinterpret_cast<const uint16_t*>(&h);
+    } else if (law == 1) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(z);
+      p = *reinterpret_cast<const uint16_t*>(&h);
+    } else {
+      p = (uint16_t)(a % 0xE000u);
+    }
+    w[i] = p;
+  }
+}
+
+struct V8 { uint32_t x[8]; };
+__device__ __forceinline__ V8 ldg8(const uint16_t* p) {
+  V8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.x[0]), "=r"(r.x[1]), "=r"(r.x[2]), "=r"(r.x[3]), "=r"(r.x[4]), "=r"(r.x[5]), "=r"(r.x[6]),
+                 "=r"(r.x[7]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void red_s(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// MODE 0: read only; 1: u32 array, word = pattern (F1's fp16 path); 2: word = pattern with the
+// bank bits XOR-scrambled by higher bits; 3: G-lane copy layout (G = 4): word = row * 32 + group *
+// 4 + (pattern & 3), row = (pattern >> 2) mod 1792 -- the conflict law of a 4-lane-shared copy
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) k_hist(const uint16_t* w, size_t nv, unsigned* out) {
+  extern __shared__ uint32_t h[];
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(h);
+  const uint32_t gb = (threadIdx.x & 31) & ~3u;
+  uint32_t acc = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  auto one = [&](uint32_t p) {
+    if (MODE == 1) red_s(base + min(p, (uint32_t)kWords - 1) * 4, 1u);
+    if (MODE == 2) {
+      const uint32_t q = min(p, (uint32_t)kWords - 1);
+      red_s(base + (q ^ ((q >> 5) & 31u) ^ ((q >> 10) & 31u)) * 4, 1u);
+    }
+    if (MODE == 4) red_s(base + ((p & 1023u) * 32 + (threadIdx.x & 31)) * 4, 1u);  // lane-private
+    if (MODE == 5) {  // lane-private 4-bit fields (8 per word), atom with return + carry check
+      const uint32_t c = ((p & 0x7FFFu) * 2u + (p >> 15)) & 8191u;
+      const uint32_t sh = (c & 7u) * 4u, inc = 1u << sh;
+      uint32_t old;
+      asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(base + ((c >> 3) * 32 + (threadIdx.x & 31)) * 4), "r"(inc) : "memory");
+      if ((~old & (15u << sh)) == 0) atomicAdd(out, 16u);
+    }
+    if (MODE == 6) {  // the same with red (no return, no check): the atomic cost alone
+      const uint32_t c = ((p & 0x7FFFu) * 2u + (p >> 15)) & 8191u;
+      red_s(base + ((c >> 3) * 32 + (threadIdx.x & 31)) * 4, 1u << ((c & 7u) * 4u));
+    }
+    if (MODE == 3) {
+      const uint32_t row = __umulhi(p >> 2, 2396745u);  // ~ (p >> 2) / 1792, cheap stand-in
+      const uint32_t r = (p >> 2) - row * 1792u;
+      red_s(base + ((r & 1791u) * 32 + gb + (p & 3u)) * 4, 1u);
+    }
+  };
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < nv; v += 2 * stride) {
+    const bool two = v + stride < nv;
+    V8 r0 = ldg8(w + 16 * v), r1;
+    if (two) r1 = ldg8(w + 16 * (v + stride));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (MODE == 0) acc ^= r0.x[q];
+      else { one(r0.x[q] & 0xFFFFu); one(r0.x[q] >> 16); }
+    }
+    if (two) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (MODE == 0) acc ^= r1.x[q];
+        else { one(r1.x[q] & 0xFFFFu); one(r1.x[q] >> 16); }
+      }
+    }
+  }
+  __syncthreads();
+  if (acc == 0x12345678u || (threadIdx.x == 0 && h[blockIdx.x] == 0xFFFFFFFFu)) atomicAdd(out, acc);
+}
+
+
+// the u32-array loop software-pipelined: the next NV vectors are loaded before the current NV are
+// counted, so every warp keeps loads in flight while it waits on its atomics
+template <int NV>
+__global__ void __launch_bounds__(1024, 1) k_hist_pf(const uint16_t* w, size_t nv, unsigned* out) {
+  extern __shared__ uint32_t h[];
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(h);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  V8 cur[NV], nxt[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+    if (v + j * stride < nv) cur[j] = ldg8(w + 16 * (v + j * stride));
+  for (; v < nv; v += NV * stride) {
+    const size_t vn = v + NV * stride;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (vn + j * stride < nv) nxt[j] = ldg8(w + 16 * (vn + j * stride));
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if (v + j * stride < nv) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          red_s(base + min(cur[j].x[q] & 0xFFFFu, (uint32_t)kWords - 1) * 4, 1u);
+          red_s(base + min(cur[j].x[q] >> 16, (uint32_t)kWords - 1) * 4, 1u);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cur[j] = nxt[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && h[blockIdx.x] == 0xFFFFFFFFu) atomicAdd(out, 1u);
+}
+
+
+// MODE 7 body: F1 nibble layout for fp16 -- lane-private 4-bit counters, 8 per word, a 28-page
+// magnitude window [mbase, mbase + 7168) per sign (positive words 0..895, negative 897..1792,
+// trash 896 / 1793), two patterns per SIMD step
+__global__ void __launch_bounds__(1024, 1) k_nib(const uint16_t* w, size_t nv, unsigned* out) {
+  extern __shared__ uint32_t h[];
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(h) + (threadIdx.x & 31) * 4;
+  const uint32_t pb2 = ((0x10000u - 0x1400u) & 0xFFFFu) * 0x10001u, lim2 = 7168u * 0x10001u;
+  uint32_t rmax = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  auto pair = [&](uint32_t x) {
+    const uint32_t y = x & 0x7FFF7FFFu;
+    const uint32_t rel = __vadd2(y, pb2);
+    const uint32_t rc = __vminu2(rel, lim2);
+    rmax = __vmaxu2(rmax, rc);
+    const uint32_t sg = (x >> 15) & 0x00010001u;
+    const uint32_t r = sg * 7176u + rc;
+    const uint32_t alo = ((r & 0x3FF8u) << 4) + base, ahi = ((r & 0x3FF80000u) >> 12) + base;
+    uint32_t ilo, ihi;
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(ilo) : "r"(0u), "r"(1u), "r"(r << 2));
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(ihi) : "r"(0u), "r"(1u), "r"(r >> 14));
+    red_s(alo, ilo);
+    red_s(ahi, ihi);
+  };
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < nv; v += 2 * stride) {
+    const bool two = v + stride < nv;
+    V8 r0 = ldg8(w + 16 * v), r1;
+    if (two) r1 = ldg8(w + 16 * (v + stride));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pair(r0.x[q]);
+    if (two) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pair(r1.x[q]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (h[blockIdx.x] == 0xFFFFFFFFu || rmax == 0x12345678u)) atomicAdd(out, 1u);
+}
+
+typedef void (*KF)(const uint16_t*, size_t, unsigned*);
+static float runk(KF k, const uint16_t* w, size_t n, unsigned* out, int sms) {
+  const size_t smem = 1794 * 128;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k<<<sms, 1024, smem>>>(w, n / 16, out);
+  float best = 1e9;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    k<<<sms, 1024, smem>>>(w, n / 16, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) printf("kernel error: %s\n", cudaGetErrorString(err));
+  return best;
+}
+template <int MODE>
+static float run(const uint16_t* w, size_t n, unsigned* out, int sms) {
+  return runk(k_hist<MODE>, w, n, out, sms);
+}
+
+int main() {
+  setvbuf(stdout, NULL, _IONBF, 0);
+  int sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const size_t n = (size_t)1 << 31;  // 2 G patterns = 4 GiB
+  uint16_t* w;
+  unsigned* out;
+  if (cudaMalloc(&w, n * 2) != cudaSuccess || cudaMalloc(&out, 4) != cudaSuccess) return 1;
+  printf("B200 SMs=%d clock(attr)=%d MHz, %zu patterns per run\n", sms, clk / 1000, n);
+  const char* laws[3] = {"fp16 N(0,.02^2)", "bf16 N(0,.02^2)", "uniform <0xE000"};
+  const char* modes[10] = {"read only", "u32 array", "u32 array, bank-scrambled", "4-lane copies",
+                          "u32 array, prefetch 1 vec", "u32 array, prefetch 2 vec", "lane-private", "lane-private 4b atom+chk", "lane-private 4b red", "nibble window (SIMD)"};
+  for (int law = 0; law < 3; ++law) {
+    gen<<<sms * 8, 256>>>(w, n, law);
+    cudaDeviceSynchronize();
+    float ms[10] = {run<0>(w, n, out, sms), run<1>(w, n, out, sms), run<2>(w, n, out, sms), run<3>(w, n, out, sms),
+                   runk(k_hist_pf<1>, w, n, out, sms), runk(k_hist_pf<2>, w, n, out, sms), run<4>(w, n, out, sms), run<5>(w, n, out, sms), run<6>(w, n, out, sms), runk(k_nib, w, n, out, sms)};
+    for (int m = 0; m < 10; ++m)
+      printf("%-17s %-27s %7.3f ms  %7.1f GB/s  %6.2f elem/clk/SM\n", laws[law], modes[m], ms[m],
+             n * 2 / (ms[m] * 1e6), n / (ms[m] * 1e-3) / sms / (clk * 1e3));
+  }
+  printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
