@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
   extern __shared__ __align__(16) double stage_mem[];
   const int cl = P.cl, crank = (int)cluster.block_rank(), t = blockIdx.x / cl, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  __shared__ double sG[K], sInvS[K], red[(kBThreads / 32) * K], part[2 * K], tot[K];
+  __shared__ double sG[K], sInvS[K], red[(kBThreads / 32) * K], part[2 * K];
   __shared__ CSet<K> cs;
   __shared__ BSet<K> bs;
   const double* sCt = cs.c;
@@ -768,8 +768,20 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
         warp_flush<K>(af, red_w);
       }
     }
-    cluster_allreduce_red<K, kBThreads / 32>(red, part, tot, it & 1, cluster);
-    if (tid < K) sG[tid] = tot[tid] + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
+    // the CTA's sums (warp order), then the cluster's (CTA order) read by the K updating threads
+    __syncthreads();
+    double* mine = part + (it & 1) * K;
+    if (tid < K) {
+      double x = 0.0;
+      for (int w = 0; w < kBThreads / 32; ++w) x += red[w * K + tid];
+      mine[tid] = x;
+    }
+    cluster.sync();
+    if (tid < K) {
+      double g = 0.0;
+      for (unsigned r = 0; r < cluster.num_blocks(); ++r) g += cluster.map_shared_rank(mine, r)[tid];
+      sG[tid] = g + (sInvS[tid] == 0.0 ? sG[tid] : 0.0);  // C_{t+1} = C_t where S_t = 0
+    }
     asm volatile("cp.async.wait_all;" ::: "memory");  // the next iteration's trajectories
     __syncthreads();
   }

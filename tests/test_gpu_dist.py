@@ -21,8 +21,24 @@ from paper_2309_00964_b200.dist import ShardedStep, allreduce_sum, shard_all  # 
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
-SIZES = [200_003, 65_536 * 2 + 7, 50_000]
-P_ = dict(bits=3, tau=1e-3, max_iter=4)
+# two configurations of the sharded step: a bf16 k=8 T=4 one on N(0, 1) weights, and a CFG4-like
+# one (fp16 N(0, 0.02^2), k=16, tau=1e-5, T=30) with 40 tensors, so that the table phase runs
+# with CFG4's cluster size (4 CTAs per tensor for fp16 when nt > 37) -- the configuration bench.py
+# splits by tensor block at N > 1 (k T >= 64)
+CONFIGS = {
+    "bf16_k8": dict(dtype=torch.bfloat16, sigma=1.0, sizes=[200_003, 65_536 * 2 + 7, 50_000],
+                    p=dict(bits=3, tau=1e-3, max_iter=4)),
+    "fp16_k16_T30": dict(dtype=torch.float16, sigma=0.02, sizes=[20_011 + 37 * i for i in range(40)],
+                         p=dict(bits=4, tau=1e-5, max_iter=30)),
+}
+SIZES = CONFIGS["bf16_k8"]["sizes"]
+P_ = CONFIGS["bf16_k8"]["p"]
+
+
+def _inputs(cfg):
+    Ws = [synth.normal_tensor(n, cfg["sigma"], cfg["dtype"], 500 + i) for i, n in enumerate(cfg["sizes"])]
+    Gs = [synth.normal_tensor(n, 1e-3, cfg["dtype"], 600 + i) for i, n in enumerate(cfg["sizes"])]
+    return Ws, Gs
 
 
 def _reduce_via_host(t: torch.Tensor):
@@ -47,24 +63,26 @@ def _max_via_host(t: torch.Tensor):
     t.copy_(h)
 
 
-def _worker(rank, world, port, q, shard_table=False):
+def _worker(rank, world, port, q, shard_table=False, cfg_name="bf16_k8"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2309_00964_b200.dist import padded_numels
+        cfg = CONFIGS[cfg_name]
         dev = torch.device("cuda", 0)
-        p = E.Params(torch.bfloat16, **P_)
-        Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
-        Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i) for i, n in enumerate(SIZES)]
-        rng = shard_all(SIZES, rank, world)
+        dt = cfg["dtype"]
+        p = E.Params(dt, **cfg["p"])
+        Ws, Gs = _inputs(cfg)
+        rng = shard_all(cfg["sizes"], rank, world)
         Wl = [w[a:b].contiguous().to(dev) for w, (a, b) in zip(Ws, rng)]
         Gl = [g[a:b].contiguous().to(dev) for g, (a, b) in zip(Gs, rng)]
         numels = [w.numel() for w in Wl]
         if shard_table:  # empty tensors pad the list to equal per-rank table-phase blocks
             numels = padded_numels(numels, world)
-            Wl += [torch.empty(0, dtype=torch.bfloat16, device=dev)] * (len(numels) - len(Wl))
-            Gl += [torch.empty(0, dtype=torch.bfloat16, device=dev)] * (len(numels) - len(Gl))
-        C0 = torch.tensor([synth.quantile_centroids(p.k, 1.0)] * len(numels), dtype=torch.float32, device=dev)
+            Wl += [torch.empty(0, dtype=dt, device=dev)] * (len(numels) - len(Wl))
+            Gl += [torch.empty(0, dtype=dt, device=dev)] * (len(numels) - len(Gl))
+        C0 = torch.tensor([synth.quantile_centroids(p.k, cfg["sigma"])] * len(numels), dtype=torch.float32,
+                          device=dev)
         plan = E.Plan(numels, p, dev)
         outs = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
         dW = [torch.empty(w.numel(), dtype=torch.float32, device=dev) for w in Wl]
@@ -88,8 +106,9 @@ def free_port():
     return port
 
 
+@pytest.mark.parametrize("cfg_name", list(CONFIGS))
 @pytest.mark.parametrize("shard_table", [False, True, "compact"])
-def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table):
+def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table, cfg_name):
     """shard_table=True: each rank runs TF/TB for its own tensor block and the ranks all-gather
     the per-tensor results; "compact": the other tensors' layout is derived
     locally and only the owners' states, trajectories and populated table pages are exchanged.
@@ -98,7 +117,7 @@ def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shard_table)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shard_table, cfg_name)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = {}
@@ -108,16 +127,18 @@ def test_two_ranks_on_one_gpu_match_single_process_oracle(shard_table):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    Ws = [synth.normal_tensor(n, 1.0, torch.bfloat16, 500 + i) for i, n in enumerate(SIZES)]
-    Gs = [synth.normal_tensor(n, 1e-3, torch.bfloat16, 600 + i) for i, n in enumerate(SIZES)]
-    k = 1 << P_["bits"]
-    C0 = np.float32(synth.quantile_centroids(k, 1.0)).astype(np.float64)
-    for t, n in enumerate(SIZES):
+    cfg = CONFIGS[cfg_name]
+    pp = cfg["p"]
+    Ws, Gs = _inputs(cfg)
+    k = 1 << pp["bits"]
+    C0 = np.float32(synth.quantile_centroids(k, cfg["sigma"])).astype(np.float64)
+    fmt = O.BF16 if cfg["dtype"] == torch.bfloat16 else O.FP16
+    for t, n in enumerate(cfg["sizes"]):
         bits = Ws[t].view(torch.int16).numpy().view(np.uint16)
-        w = O.decode16(bits, O.BF16)
-        Ct, St, _ = O.dkm_forward(w, C0, P_["tau"], P_["max_iter"])
-        Wt = O.reconstruct(w, Ct[-1], P_["tau"])
-        dW, dC = O.dkm_backward(w, Gs[t].double().numpy(), Ct, St, P_["tau"])
+        w = O.decode16(bits, fmt)
+        Ct, St, _ = O.dkm_forward(w, C0, pp["tau"], pp["max_iter"])
+        Wt = O.reconstruct(w, Ct[-1], pp["tau"])
+        dW, dC = O.dkm_backward(w, Gs[t].double().numpy(), Ct, St, pp["tau"])
         for r in range(world):
             assert np.array_equal(res[r][1][t], O.histogram(bits).astype(np.int32))  # global counts, exact
             assert np.array_equal(res[r][2][t], res[0][2][t])                        # C_T rank-identical
