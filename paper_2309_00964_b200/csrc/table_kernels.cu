@@ -17,8 +17,10 @@
 // memory; k-vector sums are reduced per thread in row order, then by warp
 // shuffles, across warps in warp order and across the cluster through DSMEM in
 // CTA order -- deterministic and identical on every CTA and every rank.
-// Sums, centroids and the backward recursion are fp64; the attention exponentials are fp32
-// on an accurately reduced argument (attention_row, R7).  Cost O(U k T), independent of N.
+// The arithmetic of one row at one iteration is fp32 (the attention on an accurately reduced
+// argument, attention_row; TB's terms re-centred on the nearest centroid, tb_row); every sum over
+// rows, the centroids, S_t and the recursion across iterations are fp64 (R7).
+// Cost O(U k T), independent of N.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
