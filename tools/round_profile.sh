@@ -7,7 +7,7 @@ TAG=${1:-r02}
 O=gpurun_out
 mkdir -p $O
 K='regex:f1_hist|tf_kernel|f2_gather|b1_bucket|tgamma_kernel|tb_kernel|tb_split|b2_dw'
-python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/${TAG}_pytest_gpu.txt
+EDKM_PARITY_REPORT=$O/${TAG}_parity_errors.json python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/${TAG}_pytest_gpu.txt
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err
 for wl in cfg2 cfg4 cfg4_b2 cfg5; do
@@ -21,6 +21,9 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k "$K" \
     --launch-skip 7 --launch-count 7 -o $O/${TAG}_full -f python bench.py --steps 1 --warmup 3 --no-e2e \
     --no-cpu-baseline --no-graph > $O/${TAG}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:tf_kernel|tgamma|tb_kernel" --launch-count 3 \
+    -o $O/${TAG}_cfg4_table -f python bench.py --workload cfg4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+    --no-graph > $O/${TAG}_ncu_cfg4_table.log 2>&1
 for tool in memcheck racecheck synccheck initcheck; do
   echo "$tool: $(compute-sanitizer --tool $tool python tools/sanitize_step.py 2>&1 | grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' | tail -1)"
 done > $O/${TAG}_sanitizer.txt
