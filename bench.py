@@ -268,8 +268,13 @@ def main():
         torch.cuda.set_device(local)
         if backend == "nccl":
             # NCCL's init lines (rank, nRanks, transports) stay visible on stderr at N > 1
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            # (the image presets NCCL_DEBUG=VERSION, whose one line NCCL writes to stdout; at INFO it
+            # honours NCCL_DEBUG_FILE, so the version and INIT lines go to stderr and stdout keeps the
+            # one JSON line)
+            if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
+                os.environ["NCCL_DEBUG"] = "INFO"
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
