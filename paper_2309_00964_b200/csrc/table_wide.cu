@@ -443,9 +443,13 @@ __global__ void __launch_bounds__(kWThreads) tb_wide_kernel(const TableArgs P) {
         pp[u] = make_float2((float)(2.0 * P.inv_tau * var), (float)ps);
       }
     }
-    for (int u = st->pbase[p] + tid; u < st->pbase[p + 1]; u += kWThreads)
-      if (!pattern_finite(u, P.wdtype) || cnt[u] == 0)
+    // NaN/Inf patterns: NaN (R10); absent finite patterns are never read (as in tb_kernel)
+    const int nf0 = P.wdtype == kBF16 ? 0x7F80 : 0x7C00;
+    for (int h = 0; h < 2; ++h) {
+      const int lo = max(st->pbase[p], h * 0x8000 + nf0), hi = min(st->pbase[p + 1], h * 0x8000 + 0x8000);
+      for (int u = lo + tid; u < hi; u += kWThreads)
         pp[u] = make_float2(__int_as_float(0x7FC00000), __int_as_float(0x7FC00000));
+    }
   }
   cluster.sync();
 }
