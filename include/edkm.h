@@ -184,9 +184,11 @@ edkm_status edkm_ipc_close(void* dev_ptr);
  *   C0     : [nt][k] fp32 initial centroids.
  *   C_out  : [nt][k] fp32 = C_T, the lookup table of the palettised weight.
  *   table  : [nt][65536] fp32, table[u] = sum_j A(v_u, C_T)[j] C_T[j] (DESIGN R2) for
- *            every pattern with counts > 0; NaN for the others.
+ *            every finite pattern with counts > 0; NaN for the NaN/Inf patterns (R10); the
+ *            entries of absent finite patterns are not written (no weight reads them).
  *   saved  : edkm_saved_bytes(nt, p) bytes, consumed by reconstruct/backward.
- * The loop runs in fp64; results are identical on every rank given equal counts. */
+ * Per-pattern attention arithmetic is fp32 and every sum over patterns, the centroids and the
+ * trajectories fp64 (DESIGN R7); results are identical on every rank given equal counts. */
 edkm_status edkm_forward(const int32_t* counts, int nt, const edkm_params* p, const float* C0, float* C_out,
                          float* table, void* saved, void* stream);
 
@@ -198,8 +200,9 @@ edkm_status edkm_forward_range(const int32_t* counts, int nt, int t0, int t1, co
                                float* C_out, float* table, void* saved, void* stream);
 
 /* TF's layout part only, for tensors [t0, t1): the populated-pattern rows and partitions, the page
- * masses, the non-finite counts, the per-weight kernels' windows (all in `saved`) and the NaN fill
- * of the W~ tables -- everything every rank derives identically from the global counts -- but no
+ * masses, the non-finite counts, the per-weight kernels' windows (all in `saved`) and the NaN
+ * entries of the NaN/Inf patterns in the W~ tables -- everything every rank derives identically
+ * from the global counts -- but no
  * iterations, no C trajectory and no W~ values.  For a table phase split by tensor (the rank that
  * does not own a tensor then receives only its C trajectory, TensorState, C_T and the populated
  * pages of its tables; dist.ShardedStep(compact_tables=True)).  table: [nt][65536] fp32. */

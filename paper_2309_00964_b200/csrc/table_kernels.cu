@@ -377,20 +377,24 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
     }
     unsigned popmask = 0;
     long long pm = 0;
+    // the non-finite patterns form aligned blocks (bf16: 128, fp16: 1,024 per sign), so a 16-aligned
+    // group is finite or not as a whole
+    const bool fin = pattern_finite(u0, P.wdtype);
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      const bool fin = pattern_finite(u0 + e, P.wdtype);
       if (fin && c[e] > 0) popmask |= 1u << e;
-      if (!fin) nonfin += c[e];
       pm += c[e];
     }
+    if (!fin) nonfin += pm;
     if (sign_split) {  // one signed page = 256 patterns = 16 threads (the ranges are page-aligned)
 #pragma unroll
       for (int o = 8; o; o >>= 1) pm += __shfl_xor_sync(0xffffffffu, pm, o);
       if ((lane & 15) == 0 && in) P.page_cnt[(int64_t)t * 256 + (u0 >> 8)] = pm;
     }
-    if (in) {
-      // NaN fill (populated entries are overwritten in phase 3); hard index 0 for non-finite patterns
+    if (in && !fin) {
+      // NaN/Inf patterns: W~ = NaN, hard index 0 (R10).  Finite patterns are written in phase 3 when
+      // populated; absent ones are never read (round 1 NaN-filled all 65,536 entries of the three
+      // tables of every tensor: 104 MB of stores per CFG3 step)
       const float nanf = __int_as_float(0x7FC00000);
       float4* t4 = reinterpret_cast<float4*>(tab + u0);
 #pragma unroll
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
       uint4* h4 = reinterpret_cast<uint4*>(tab16 + u0);
       h4[0] = make_uint4(n16, n16, n16, n16);
       h4[1] = make_uint4(n16, n16, n16, n16);
-      *reinterpret_cast<uint4*>(idx + u0) = make_uint4(0, 0, 0, 0);  // populated entries set in phase 3
+      *reinterpret_cast<uint4*>(idx + u0) = make_uint4(0, 0, 0, 0);
     }
     // block exclusive scan of the per-thread populated counts
     const int np = __popc(popmask);

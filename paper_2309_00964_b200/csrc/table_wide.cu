@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
     const bool fin = pattern_finite(u, P.wdtype);
     const bool pop = in && fin && c > 0;
     if (!fin) nonfin += c;
-    if (in) {
-      idx[u] = 0;  // populated entries set in phase 3
+    if (in && !fin) {  // NaN/Inf patterns (R10); populated finite ones are set in phase 3, absent ones never read
+      idx[u] = 0;
       tab[u] = nanf;
       tab16[u] = nan16(P.wdtype);
     }
