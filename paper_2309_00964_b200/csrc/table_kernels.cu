@@ -310,11 +310,23 @@ struct RowStage {
   __device__ __forceinline__ double& psi(int r) const { return r < ns ? spsi[r] : gpsi[r]; }
   __device__ __forceinline__ float vf(int r) const { return r < ns ? sv[r] : decode16f(rows[r], wdtype); }
   __device__ __forceinline__ float nf(int r) const { return (float)(r < ns ? sn[r] : cnt[rows[r]]); }
+  // four rows per thread per step: their pattern loads, then their count gathers, are issued
+  // together (a dependent rows[r] -> cnt[u] pair per row measured 12% of CFG3's TB)
   __device__ void stage() {
-    for (int r = threadIdx.x; r < nr && r < ns; r += blockDim.x) {
-      const uint32_t u = rows[r];
-      sv[r] = decode16f(u, wdtype);
-      sn[r] = cnt[u];
+    const int lim = min(nr, ns), bd = blockDim.x;
+    for (int r0 = threadIdx.x; r0 < lim; r0 += 4 * bd) {
+      uint32_t u[4];
+      int32_t c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = r0 + q * bd < lim ? (uint32_t)rows[r0 + q * bd] : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = r0 + q * bd < lim ? cnt[u[q]] : 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (r0 + q * bd < lim) {
+          sv[r0 + q * bd] = decode16f(u[q], wdtype);
+          sn[r0 + q * bd] = c[q];
+        }
     }
     __syncthreads();
   }
@@ -357,6 +369,8 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   }
   const int base = s_pb[crank], end = s_pb[crank + 1];
   uint16_t* rows = P.rows + (int64_t)t * kPatterns + base;
+  float* stage_v = reinterpret_cast<float*>(stage_mem);                // [kStage] value v_u
+  int32_t* stage_n = reinterpret_cast<int32_t*>(stage_mem) + kStage;  // [kStage] count n_u
 
   // ---- 1. compact populated finite patterns of this partition (ascending u), 16 per thread per step;
   //         non-finite counts, NaN-fill of the W~ tables
@@ -422,10 +436,17 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
       btot += x;
     }
     int pos = nr + woff + incl - np;
-    while (popmask) {
-      const int e = __ffs(popmask) - 1;
-      popmask &= popmask - 1;
-      rows[pos++] = (uint16_t)(u0 + e);
+    if (popmask) {  // the rows, and their value and count staged in shared memory (no re-read)
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (popmask & (1u << e)) {
+          rows[pos] = (uint16_t)(u0 + e);
+          if (pos < kStage) {
+            stage_v[pos] = decode16f(u0 + e, P.wdtype);
+            stage_n[pos] = c[e];
+          }
+          ++pos;
+        }
     }
     nr += btot;
     __syncthreads();
@@ -449,9 +470,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
     table_windows(P.page_cnt + (int64_t)t * 256, st, crank);
     return;
   }
-  RowStage R{rows, cnt, reinterpret_cast<float*>(stage_mem), reinterpret_cast<int32_t*>(stage_mem) + kStage, nullptr,
-             nullptr, nr, P.wdtype, kStage};
-  R.stage();
+  RowStage R{rows, cnt, stage_v, stage_n, nullptr, nullptr, nr, P.wdtype, kStage};  // staged by the compaction
 
   // ---- 2. unrolled centroid updates
   const int stride_c = (P.max_iter + 1) * K, stride_s = (P.max_iter > 0 ? P.max_iter : 1) * K;
