@@ -453,14 +453,17 @@ def test_uniquify_lane_private_folds(case, ctas):
     assert np.array_equal(counts.cpu().numpy()[0], O.histogram(b).astype(np.int32))
 
 
-def test_nonfinite_patterns_flagged_and_excluded():
+@pytest.mark.parametrize("dtype,bits", [(torch.bfloat16, 3), (torch.float16, 4), (torch.bfloat16, 6)])
+def test_nonfinite_patterns_flagged_and_excluded(dtype, bits):
+    """NaN/Inf weights: counted, excluded from clustering, W~ and dW NaN (R10) -- for bf16 and fp16
+    (different non-finite pattern blocks) and for the warp-per-row kernels (k = 64)."""
     n = 100_000
-    W = synth.normal_tensor(n, 1.0, torch.bfloat16, 21)
+    W = synth.normal_tensor(n, 1.0, dtype, 21)
     bad = torch.tensor([5, 77, 1000, 99_999])
-    W[bad] = torch.tensor([float("nan"), float("inf"), -float("inf"), float("nan")], dtype=torch.bfloat16)
-    G = synth.normal_tensor(n, 1e-3, torch.bfloat16, 22)
-    C0 = synth.quantile_centroids(8, 1.0)
-    p = E.Params(torch.bfloat16, 3, 1e-3, 5)
+    W[bad] = torch.tensor([float("nan"), float("inf"), -float("inf"), float("nan")], dtype=dtype)
+    G = synth.normal_tensor(n, 1e-3, dtype, 22)
+    C0 = synth.quantile_centroids(1 << bits, 1.0)
+    p = E.Params(dtype, bits, 1e-3, 5)
     gpu = run_gpu([W], [G], [C0], p)
     wb = bits_of(W)
     ref = oracle_dense(wb, G.double().numpy(), C0, p)
