@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   int32_t* stage_n = reinterpret_cast<int32_t*>(stage_mem) + kStage;  // [kStage] count n_u
 
   // ---- 1. compact populated finite patterns of this partition (ascending u), 16 per thread per step;
-  //         non-finite counts, NaN-fill of the W~ tables
+  //         non-finite counts, NaN entries of the non-finite patterns in the W~ tables
   int nr = 0;
   long long nonfin = 0;
   for (int off = 0; off < end - base; off += kFThreads * 16) {

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kWThreads) tf_wide_kernel(const TableArgs P) {
   uint8_t* idx = P.idx8 + (int64_t)t * kPatterns;
   const float nanf = __int_as_float(0x7FC00000);
 
-  // ---- 1. compaction of this partition (one pattern per thread per step), NaN fill
+  // ---- 1. compaction of this partition (one pattern per thread per step), NaN entries of the non-finite patterns
   int nr = 0;
   long long nonfin = 0;
   for (int off = 0; off < end - base; off += kWThreads) {
