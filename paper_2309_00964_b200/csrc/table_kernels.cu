@@ -101,6 +101,7 @@ struct CSet {
       if (sv[pos + st - 1] < vf) pos += st;
     // candidates sv[pos-1], sv[pos]
     const int lo = pos > 0 ? pos - 1 : 0;
+    EDKM_BCHECK(pos >= 0 && pos < K);
     return (fabsf(vf - sv[lo]) <= fabsf(vf - sv[pos])) ? sidx[lo] : sidx[pos];
   }
 };
@@ -305,9 +306,15 @@ struct RowStage {
   double* spsi;  // [kStage] psi accumulator (TB)
   double* gpsi;  // global psi for r >= kStage
   int nr, wdtype, ns;  // ns: staged capacity
-  __device__ __forceinline__ double v(int r) const { return r < ns ? (double)sv[r] : decode16(rows[r], wdtype); }
+  __device__ __forceinline__ double v(int r) const {
+    EDKM_BCHECK(r >= 0 && r < nr);
+    return r < ns ? (double)sv[r] : decode16(rows[r], wdtype);
+  }
   __device__ __forceinline__ double n(int r) const { return (double)(r < ns ? sn[r] : cnt[rows[r]]); }
-  __device__ __forceinline__ double& psi(int r) const { return r < ns ? spsi[r] : gpsi[r]; }
+  __device__ __forceinline__ double& psi(int r) const {
+    EDKM_BCHECK(r >= 0 && r < nr);
+    return r < ns ? spsi[r] : gpsi[r];
+  }
   __device__ __forceinline__ float vf(int r) const { return r < ns ? sv[r] : decode16f(rows[r], wdtype); }
   __device__ __forceinline__ float nf(int r) const { return (float)(r < ns ? sn[r] : cnt[rows[r]]); }
   // four rows per thread per step: their pattern loads, then their count gathers, are issued
@@ -324,6 +331,7 @@ struct RowStage {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (r0 + q * bd < lim) {
+          EDKM_BCHECK(r0 + q * bd < ns && u[q] < (uint32_t)kPatterns);
           sv[r0 + q * bd] = decode16f(u[q], wdtype);
           sn[r0 + q * bd] = c[q];
         }
@@ -440,6 +448,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
 #pragma unroll
       for (int e = 0; e < 16; ++e)
         if (popmask & (1u << e)) {
+          EDKM_BCHECK(pos < end - base && u0 + e < end);
           rows[pos] = (uint16_t)(u0 + e);
           if (pos < kStage) {
             stage_v[pos] = decode16f(u0 + e, P.wdtype);
@@ -459,6 +468,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
     long long s = 0;
     for (int w = 0; w < (kFThreads / 32); ++w) s += s_nf[w];
     st->nonfinite[crank] = s;
+    EDKM_BCHECK(nr >= 0 && nr <= end - base);
     st->nrows[crank] = nr;
     if (crank == 0) {
       st->cl = cl;
@@ -511,7 +521,10 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
         }
       };
       if (r1 <= R.ns) {  // staged rows (the usual case): shared memory only
-        for (int r = rb + lane; r < r1; r += kFThreads) row(R.sv[r], (float)R.sn[r]);
+        for (int r = rb + lane; r < r1; r += kFThreads) {
+          EDKM_BCHECK(r < R.ns && r < nr);
+          row(R.sv[r], (float)R.sn[r]);
+        }
       } else {
         for (int r = rb + lane; r < r1; r += kFThreads) row(R.vf(r), R.nf(r));
       }
@@ -565,6 +578,7 @@ __global__ void __launch_bounds__(kFThreads, kMinBlocks) tf_kernel(const TableAr
   // ---- 3. per populated pattern: W~ (fp32 and 16-bit), hard index vs the fp32 C_out
   for (int r = tid; r < nr; r += kFThreads) {
     const uint32_t u = rows[r];
+    EDKM_BCHECK((int)u >= base && (int)u < end);
     const double v = R.v(r);
     int best = 0;
     double bd = (v - sCf[0]) * (v - sCf[0]);
@@ -620,7 +634,10 @@ __global__ void __launch_bounds__(kFThreads, K <= 8 ? 4 : EDKM_TG_MB16) tgamma_k
 #pragma unroll
       for (int q = 0; q < NB; ++q) uq[q] = r0 + q * kFThreads < nr ? (uint32_t)rows[r0 + q * kFThreads] : 0u;
 #pragma unroll
-      for (int q = 0; q < NB; ++q) Bq[q] = r0 + q * kFThreads < nr ? Bt[uq[q]] : 0.0;
+      for (int q = 0; q < NB; ++q) {
+        EDKM_BCHECK(uq[q] < (uint32_t)kPatterns);
+        Bq[q] = r0 + q * kFThreads < nr ? Bt[uq[q]] : 0.0;
+      }
 #pragma unroll 1
       for (int q = 0; q < NB; ++q) {
         const uint32_t u = uq[q];
@@ -748,6 +765,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
   __shared__ __align__(16) double sTr[2][3 * K];
   auto fetch = [&](int it, int buf) {
     if (tid < 3 * K) {
+      EDKM_BCHECK(buf == 0 || buf == 1);
       const double* src = tid < K ? ctraj + (int64_t)it * K + tid
                                   : tid < 2 * K ? ctraj + (int64_t)(it + 1) * K + (tid - K) : straj + (int64_t)it * K + (tid - 2 * K);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(&sTr[buf][tid])), "l"(src) : "memory");
@@ -784,6 +802,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
         const int r1 = min(nr, rb + kRowFlush * kBThreads);
         if (one && r1 <= R.ns) {  // staged rows (the usual case)
           for (int r = rb + lane; r < r1; r += kBThreads) {
+            EDKM_BCHECK(r < R.ns && r < R.nr);
             double& ps = kPsiShared ? R.spsi[r] : gpsi[r];
             const double ps_old = it == T - 1 ? 0.0 : ps;  // issued before the row's arithmetic
             ps = ps_old + (double)tb_row<K>(R.sv[r], (float)R.sn[r], cs, bs, h1f, af);
@@ -828,6 +847,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
     const int nr = one ? R.nr : st->nrows[p];
     for (int r = tid; r < nr; r += kBThreads) {
       const uint32_t u = rows[r];
+      EDKM_BCHECK((int)u >= st->pbase[p] && (int)u < st->pbase[p + 1]);
       const double v = one ? R.v(r) : decode16(u, P.wdtype);
       float Af[K];
       attention_row<K>((float)v, cs, Af);
@@ -847,7 +867,10 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) tb_kernel(const TableAr
     const int nf0 = P.wdtype == kBF16 ? 0x7F80 : 0x7C00;  // first non-finite pattern of each sign
     for (int h = 0; h < 2; ++h) {
       const int lo = max(st->pbase[p], h * 0x8000 + nf0), hi = min(st->pbase[p + 1], h * 0x8000 + 0x8000);
-      for (int u = lo + tid; u < hi; u += kBThreads) pp[u] = nan2;
+      for (int u = lo + tid; u < hi; u += kBThreads) {
+        EDKM_BCHECK(u >= st->pbase[p] && u < st->pbase[p + 1] && !pattern_finite(u, P.wdtype));
+        pp[u] = nan2;
+      }
     }
   }
   cluster.sync();
