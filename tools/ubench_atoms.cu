@@ -181,6 +181,48 @@ __global__ void __launch_bounds__(1024, 1) k_nib(const uint16_t* w, size_t nv, u
   if (threadIdx.x == 0 && (h[blockIdx.x] == 0xFFFFFFFFu || rmax == 0x12345678u)) atomicAdd(out, 1u);
 }
 
+
+// G = 4 copies of 8-bit counters (the fp16 F1 candidate): lane group g = lane / 4 owns banks 4g..4g+3;
+// counter c = rot1(p) - 2 * mbase over a 56-page magnitude window (28,672 counters of a copy = 7,168
+// words = 4 banks x 1,792 rows), byte c & 3 of word (row c >> 4, bank 4g + ((c >> 2) & 3))
+__global__ void __launch_bounds__(1024, 1) k_g4b(const uint16_t* w, size_t nv, unsigned* out) {
+  extern __shared__ uint32_t h[];
+  for (int i = threadIdx.x; i < 1793 * 32; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t gbase = (uint32_t)__cvta_generic_to_shared(h) + ((threadIdx.x & 31) >> 2) * 16;
+  const uint32_t nb2 = ((0x10000u - 2u * 0u) & 0xFFFFu) * 0x10001u, lim2 = 28672u * 0x10001u;  // mbase = 0
+  uint32_t rmax = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  auto pair = [&](uint32_t x) {
+    // rotate each half left by one: (mag << 1) | sign
+    uint32_t z;
+    asm("lop3.b32 %0, %1, %2, 0xFFFEFFFE, 0xE4;" : "=r"(z) : "r"(x << 1), "r"(x >> 15));
+    const uint32_t c2 = __vminu2(__vadd2(z, nb2), lim2);
+    rmax = __vmaxu2(rmax, c2);
+    const uint32_t clo = c2 & 0xFFFFu, chi = c2 >> 16;
+    const uint32_t alo = ((clo >> 4) << 7) + ((clo & 12u) | gbase);
+    const uint32_t ahi = ((chi >> 4) << 7) + ((chi & 12u) | gbase);
+    uint32_t ilo, ihi;
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(ilo) : "r"(0u), "r"(1u), "r"(clo << 3));
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(ihi) : "r"(0u), "r"(1u), "r"(chi << 3));
+    red_s(alo, ilo);
+    red_s(ahi, ihi);
+  };
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < nv; v += 2 * stride) {
+    const bool two = v + stride < nv;
+    V8 r0 = ldg8(w + 16 * v), r1;
+    if (two) r1 = ldg8(w + 16 * (v + stride));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pair(r0.x[q]);
+    if (two) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pair(r1.x[q]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (h[blockIdx.x] == 0xFFFFFFFFu || rmax == 0x12345678u)) atomicAdd(out, 1u);
+}
+
 typedef void (*KF)(const uint16_t*, size_t, unsigned*);
 static float runk(KF k, const uint16_t* w, size_t n, unsigned* out, int sms) {
   const size_t smem = 1794 * 128;
@@ -219,14 +261,14 @@ int main() {
   if (cudaMalloc(&w, n * 2) != cudaSuccess || cudaMalloc(&out, 4) != cudaSuccess) return 1;
   printf("B200 SMs=%d clock(attr)=%d MHz, %zu patterns per run\n", sms, clk / 1000, n);
   const char* laws[3] = {"fp16 N(0,.02^2)", "bf16 N(0,.02^2)", "uniform <0xE000"};
-  const char* modes[10] = {"read only", "u32 array", "u32 array, bank-scrambled", "4-lane copies",
-                          "u32 array, prefetch 1 vec", "u32 array, prefetch 2 vec", "lane-private", "lane-private 4b atom+chk", "lane-private 4b red", "nibble window (SIMD)"};
+  const char* modes[11] = {"read only", "u32 array", "u32 array, bank-scrambled", "4-lane copies",
+                          "u32 array, prefetch 1 vec", "u32 array, prefetch 2 vec", "lane-private", "lane-private 4b atom+chk", "lane-private 4b red", "nibble window (SIMD)", "4-lane copies, 8-bit (fp16 F1)"};
   for (int law = 0; law < 3; ++law) {
     gen<<<sms * 8, 256>>>(w, n, law);
     cudaDeviceSynchronize();
-    float ms[10] = {run<0>(w, n, out, sms), run<1>(w, n, out, sms), run<2>(w, n, out, sms), run<3>(w, n, out, sms),
-                   runk(k_hist_pf<1>, w, n, out, sms), runk(k_hist_pf<2>, w, n, out, sms), run<4>(w, n, out, sms), run<5>(w, n, out, sms), run<6>(w, n, out, sms), runk(k_nib, w, n, out, sms)};
-    for (int m = 0; m < 10; ++m)
+    float ms[11] = {run<0>(w, n, out, sms), run<1>(w, n, out, sms), run<2>(w, n, out, sms), run<3>(w, n, out, sms),
+                   runk(k_hist_pf<1>, w, n, out, sms), runk(k_hist_pf<2>, w, n, out, sms), run<4>(w, n, out, sms), run<5>(w, n, out, sms), run<6>(w, n, out, sms), runk(k_nib, w, n, out, sms), runk(k_g4b, w, n, out, sms)};
+    for (int m = 0; m < 11; ++m)
       printf("%-17s %-27s %7.3f ms  %7.1f GB/s  %6.2f elem/clk/SM\n", laws[law], modes[m], ms[m],
              n * 2 / (ms[m] * 1e6), n / (ms[m] * 1e-3) / sms / (clk * 1e3));
   }
