@@ -325,7 +325,12 @@ def main():
     # edkm_comm_allreduce / _allgather on the step's stream); EDKM_COMM=torch uses torch.distributed
     comm = None
     if distributed and backend == "nccl" and os.environ.get("EDKM_COMM", "lib") == "lib":
-        comm = E.Comm()
+        try:
+            comm = E.Comm()
+        except Exception as e:  # every rank fails alike (same library, same NCCL): torch's NCCL instead
+            print(f"bench: libedkm.so NCCL comm unavailable ({e}); collectives via torch.distributed",
+                  file=sys.stderr)
+            comm = None
 
     def allreduce(t, op=None):
         op = dist.ReduceOp.SUM if op is None else op
