@@ -304,6 +304,36 @@ def test_heavy_tailed_gradients_cfg2_tensor(kind):
     assert normwise(gpu["dW"][0], dw_ref) <= TOL
 
 
+@pytest.mark.parametrize("dtype,bits,lo,hi,n", [(torch.bfloat16, 3, -40, 12, 60_000),
+                                                  (torch.float16, 4, -10, 4, 200_000)])
+def test_rows_beyond_the_shared_stage(dtype, bits, lo, hi, n):
+    """38 tensors (so the table kernels run CFG3/CFG4's cluster size: 2 CTAs per bf16 tensor, 4 per
+    fp16 tensor) whose weights are log-uniform over many binades, so every CTA holds more populated
+    patterns than it stages in shared memory (4,608 bf16 / 6,400 fp16 rows): the rows beyond the
+    stage take the global-memory path in TF, TGAMMA and TB (value, count and psi).  C_0: the
+    quantiles of N(0, 2^2) (well separated), tau = 1e-2."""
+    nt = 38
+    rng = np.random.default_rng(7)
+    Ws = []
+    for i in range(nt):
+        x = np.exp2(rng.uniform(lo, hi, n)) * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        Ws.append(torch.from_numpy(x).to(dtype))
+    Gs = [synth.normal_tensor(n, 1e-3, dtype, 900 + i) for i in range(nt)]
+    C0s = [synth.quantile_centroids(1 << bits, 2.0)] * nt
+    p = E.Params(dtype, bits, 1e-2, 3)
+    gpu = run_gpu(Ws, Gs, C0s, p)
+    stage = 4608 if dtype == torch.bfloat16 else 6400
+    cl = 2 if dtype == torch.bfloat16 else 4
+    beyond = 0
+    for t in range(nt):
+        wb = bits_of(Ws[t])
+        beyond += np.unique(wb).size > cl * stage
+        if t % 6 == 0:  # the dense oracle on every sixth tensor (each one runs the same kernels)
+            ref = oracle_dense(wb, Gs[t].double().numpy(), C0s[t], p)
+            check_tensor(gpu, t, wb, Gs[t].double().numpy(), ref, p)
+    assert beyond == nt  # every tensor has rows beyond its CTAs' stages
+
+
 def test_many_ragged_tensors_and_empty():
     sizes = [0, 1, 17, 4097, 65536 * 3 + 5, 0, 250_001, 2, 31, 33]
     p = E.Params(torch.bfloat16, 3, 1e-3, 4)
