@@ -7,8 +7,10 @@ One step = the whole hot path over every tensor of the workload (S1):
 F1 uniquify -> [counts all-reduce] -> TF forward iterations -> F2 reconstruct (W~, bf16)
 -> B1 buckets + gamma_T -> [gamma all-reduce] -> TB reverse loop + B2 dW (bf16).
 N=1 runs BASELINE.json's metric configuration (configs[2], full LLaMA-7B: 226 tensors,
-6,738,149,376 weights) on one B200; under torchrun every rank holds a contiguous slice of
-every tensor -- total work fixed, so "scaling": "strong".
+6,738,149,376 weights) on one B200; under torchrun the model is sharded by tensor (whole
+tensors per rank, balanced longest-first: independent clustering problems, no data-path
+exchange; EDKM_SHARD=slice: the contiguous slice of every tensor, with the count and
+gamma all-reduces) -- total work fixed, so "scaling": "strong".
 Prints ONE JSON line on rank 0.  Timing: W warm-up steps, then K steps bracketed by
 barrier + synchronize, CUDA events on the launching stream, max over ranks.  Inputs
 (27 GB of W and G per step) exceed the 126 MB L2, so no flush is needed.
@@ -162,7 +164,7 @@ def calibrate_cpu(wl, seconds, nthreads):
     return max(n0, int(n0 * seconds / max(dt, 1e-6)))
 
 
-def cpu_baseline(wl, seconds, gpu_result=None, fetch=None):
+def cpu_baseline(wl, seconds, gpu_result=None, fetch=None, tensors=None):
     """Dense oracle over whole tensors of layer 0 (q, k, v, ...) in order until ~`seconds` elapse, on
     every host core; then the same oracle on ONE thread over a 1M-weight sample.  `gpu_result(t)` gives
     the bench step's own outputs for tensor t (C_T, dC_0 and this rank's slice of W~, dW); they are
@@ -171,7 +173,7 @@ def cpu_baseline(wl, seconds, gpu_result=None, fetch=None):
     import numpy as np
     cores = len(os.sched_getaffinity(0))
     done, names, refs, tt = 0, [], {}, 0.0
-    for t in range(1, len(wl.shapes)):
+    for t in (range(1, len(wl.shapes)) if tensors is None else tensors):
         n = wl.shapes[t][1] * wl.shapes[t][2]
         b, G, C0 = cpu_sample(wl, n, seed_t=t)
         if fetch is not None:
@@ -252,7 +254,7 @@ def main():
     from paper_2309_00964_b200 import build as B
     from paper_2309_00964_b200 import edkm as E
     from paper_2309_00964_b200 import synth
-    from paper_2309_00964_b200.dist import exchange_counts_compact, shard_range
+    from paper_2309_00964_b200.dist import assign_tensors, exchange_counts_compact, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -288,9 +290,19 @@ def main():
     p = E.Params(wl.wdtype, wl.bits, wl.tau, wl.max_iter, wl.eps)
 
     # ---- synthetic inputs, resident in HBM (this rank's slice of every tensor)
+    # Sharding at N > 1 (EDKM_SHARD): "tensor" (default while the largest tensor fits a rank's share):
+    # whole tensors per rank (dist.assign_tensors, longest-first greedy), independent clustering
+    # problems (one C per tensor, R12), so the step has no data-path exchange and no replicated table
+    # phase; "slice": the contiguous slice of every tensor with the count and gamma all-reduces.
+    all_n = [r * c for _, r, c in wl.shapes]
+    smode = os.environ.get("EDKM_SHARD", "auto")
+    if smode == "auto":
+        smode = "tensor" if world > 1 and max(all_n) <= sum(all_n) / world else "slice"
+    tensor_mode = smode == "tensor"
+    owned = assign_tensors(all_n, world)[rank] if tensor_mode else list(range(len(all_n)))
     Ws, Gs, numels = [], [], []
-    for t, (_, r, c) in enumerate(wl.shapes):
-        lo, hi = shard_range(r * c, rank, world)
+    for t in owned:
+        lo, hi = (0, all_n[t]) if tensor_mode else shard_range(all_n[t], rank, world)
         w = synth.weights(wl, t, dev)[lo:hi].contiguous()
         g = synth.grads(wl, t, dev)[lo:hi].contiguous()
         Ws.append(w)
@@ -305,7 +317,7 @@ def main():
     # the estimated split (own block TF + TB ~0.18 ms, layout pass ~0.03, five all-gathers ~0.1) saves
     # ~0.04 ms of ~0.38; EDKM_SHARD_TABLE=1 forces the split, 0 disables it.
     tmode = os.environ.get("EDKM_SHARD_TABLE", "auto")
-    shard = tmode == "1" or (world > 1 and tmode == "auto" and wl.k * wl.max_iter >= 64)
+    shard = not tensor_mode and (tmode == "1" or (world > 1 and tmode == "auto" and wl.k * wl.max_iter >= 64))
     if shard:
         from paper_2309_00964_b200.dist import allgather_blocks, padded_numels
         npad = len(padded_numels(numels, world)) - len(numels)
@@ -367,14 +379,17 @@ def main():
     # one mid-step host read of the page mask, and that sync measured 0.24 ms alone but ~1-1.6 ms per
     # step while nvidia-smi samples the clocks (bench at N=1 under torchrun), more than the ~0.1 ms
     # it can save on a 59 MB NVLink all-reduce at N = 8
-    compact = distributed and os.environ.get("EDKM_COMPACT", "0") == "1"
+    compact = distributed and not tensor_mode and os.environ.get("EDKM_COMPACT", "0") == "1"
     via = "libedkm.so's NCCL comm (edkm_comm_*)" if comm is not None else f"torch.distributed ({backend})"
     nv, exchange = None, (f"counts: {'page-compact ' if compact else ''}int32 all-reduce; gamma: fp64 all-reduce; "
                           f"via {via}")
+    if tensor_mode:
+        exchange = ("none: each rank clusters whole tensors (independent problems, one C per tensor, R12); "
+                    f"only the step time's max over ranks crosses them (via {via})")
     # the NVLS-fused count exchange (multimem reductions inside F1) has not yet run on NVSwitch
     # hardware: opt-in (EDKM_NVLS=1) until it has been validated there
     mode = os.environ.get("EDKM_NVLS", "0")
-    if (world > 1 and mode != "0") or mode == "emulate":  # emulate: the protocol on plain memory, one rank
+    if not tensor_mode and ((world > 1 and mode != "0") or mode == "emulate"):  # emulate: plain memory, one rank
         from paper_2309_00964_b200.dist import NvlsCounts
         try:
             nv = NvlsCounts(len(Ws), dev, emulate=mode == "emulate")
@@ -421,8 +436,8 @@ def main():
             mark(1)
             if compact:                      # exchange 1 (N > 1), populated pages only
                 ss.page_list = exchange_counts_compact(plan, allreduce, allreduce_max)
-            else:
-                allreduce(plan.counts)       # exchange 1 (N > 1)
+            elif not tensor_mode:
+                allreduce(plan.counts)       # exchange 1 (N > 1, slices)
         mark(2)
         if shard:
             plan.forward_range(t0, t1, C0)   # TF, this rank's tensor block
@@ -446,7 +461,8 @@ def main():
         mark(5)
         plan.backward_gamma()                # TGAMMA
         mark(6)
-        allreduce(plan.gamma)                # exchange 2 (N > 1)
+        if not tensor_mode:
+            allreduce(plan.gamma)            # exchange 2 (N > 1, slices)
         mark(7)
         if shard:
             plan.backward_table_range(t0, t1)  # TB, this rank's tensor block
@@ -494,7 +510,7 @@ def main():
     # N > 1: C_T and dC_0 must be bit-identical on every rank ("weights are identical in each
     # learner"): all-gather a hash of their bytes and fail on any mismatch
     rank_identical = None
-    if distributed:
+    if distributed and not tensor_mode:  # (by tensor, every C_T / dC_0 is computed on one rank only)
         import hashlib
         hsh = hashlib.sha256(plan.C_out.cpu().numpy().tobytes() + plan.dC0.cpu().numpy().tobytes()).digest()[:8]
         mine = torch.tensor([int.from_bytes(hsh, "little", signed=True)], dtype=torch.int64)
@@ -542,7 +558,8 @@ def main():
         torch.cuda.synchronize()
 
         from paper_2309_00964_b200.pipeline import HostPipeline
-        pipe = HostPipeline(numels, p, dev, n_groups=args.e2e_groups, allreduce=allreduce if distributed else None,
+        pipe = HostPipeline(numels, p, dev, n_groups=args.e2e_groups,
+                            allreduce=allreduce if distributed and not tensor_mode else None,
                             buffers=(Ws, Gs, Wt, dW))
 
         def e2e_step():
@@ -623,10 +640,14 @@ def main():
                                f"{'bf16' if wl.wdtype == torch.bfloat16 else 'fp16'} N(0,{wl.sigma}^2), "
                                f"b={wl.bits} (k={wl.k}), tau={wl.tau}, T={wl.max_iter}",
                    "tensors": len(wl.shapes), "weights": n_total, "bits": wl.bits, "tau": wl.tau,
-                   "iters": wl.max_iter, "parallelism": f"slices{world}", "exchange": exchange,
-                   "table_phase": ("split by tensor block + " + ("page-compact exchange" if compact and nv is None
-                                                                  else "all-gather") if shard
+                   "iters": wl.max_iter, "parallelism": f"{'tensors' if tensor_mode else 'slices'}{world}",
+                   "exchange": exchange,
+                   "table_phase": ("this rank's own tensors only" if tensor_mode and world > 1 else
+                                   "split by tensor block + " + ("page-compact exchange" if compact and nv is None
+                                                                 else "all-gather") if shard
                                    else "replicated on every rank"),
+                   "rank_weights": ([sum(all_n[t] for t in o) for o in assign_tensors(all_n, world)]
+                                    if tensor_mode and world > 1 else None),
                    "arith": f"{w16} I/O; exact integer F1/B1 sums, fp32 B2 FMA; table phase: fp32 per row "
                             "(ex2.approx), fp64 sums over rows, centroids and trajectories",
                    "l2": "no flush: 27 GB of W and G per step >> 126 MB L2"},
@@ -634,15 +655,19 @@ def main():
         "clocks": clk.summary(), "roofline": roof, "table_roofline": table_roof, "e2e": e2e, "cuda_graph": graph,
     }
     if not args.no_cpu_baseline:  # rank 0 (at N > 1 too): the oracle on the host cores + the step's parity
-        def gpu_result(t):
-            lo, hi = shard_range(wl.shapes[t][1] * wl.shapes[t][2], rank, world)
-            return {"C": plan.C_out[t].cpu().numpy(), "dC0": plan.dC0[t].cpu().numpy(), "slice": (lo, hi),
-                    "Wt": Wt[t].double().cpu().numpy(), "dW": dW[t].double().cpu().numpy()}
+        def gpu_result(t):  # t: the global tensor index; i: its index in this rank's plan
+            i = owned.index(t)
+            lo, hi = (0, all_n[t]) if tensor_mode else shard_range(all_n[t], rank, world)
+            return {"C": plan.C_out[i].cpu().numpy(), "dC0": plan.dC0[i].cpu().numpy(), "slice": (lo, hi),
+                    "Wt": Wt[i].double().cpu().numpy(), "dW": dW[i].double().cpu().numpy()}
         def fetch(t):  # the bench's own data of tensor t, whole (CUDA generator, as above)
             import numpy as np
             return (synth.weights(wl, t, dev).cpu().view(torch.int16).numpy().view(np.uint16),
                     synth.grads(wl, t, dev).double().cpu().numpy())
-        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds, gpu_result, fetch)
+        # the oracle's tensors: layer 0 onwards (as at N = 1), or rank 0's own tensors by size when by tensor
+        order = (sorted((t for t in owned if t > 0), key=lambda t: (all_n[t], t)) if tensor_mode and world > 1
+                 else range(1, len(wl.shapes)))
+        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds, gpu_result, fetch, tensors=order)
     print(json.dumps(out))
     if comm is not None:
         comm.close()

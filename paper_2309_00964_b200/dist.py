@@ -1,6 +1,10 @@
 """Multi-process orchestration of the eDKM step (one process per GPU, P:79 sharding).
 
-Every rank holds the contiguous slice [floor(r n / P), floor((r+1) n / P)) of every
+Two ways to shard (the north star: "by tensor and by contiguous slices").  By tensor
+(`assign_tensors`, bench.py's default at N > 1 while the largest tensor fits a rank's share):
+every rank clusters whole tensors, which are independent problems, so nothing crosses
+ranks in the data path.  By slice (below; the paper's sharding of the index list, and the
+only way when one tensor outweighs a rank's share): every rank holds the contiguous slice [floor(r n / P), floor((r+1) n / P)) of every
 tensor (the paper shards the index list over learners; here the weights
 themselves are sliced, so only histograms and k-vectors move).  The path has two
 real exchange steps, both all-reduces over the process group (NCCL on B200):
@@ -46,6 +50,23 @@ def shard_range(n: int, rank: int, world: int) -> tuple:
 
 def shard_all(numels, rank: int, world: int):
     return [shard_range(n, rank, world) for n in numels]
+
+
+def assign_tensors(numels, world: int):
+    """Whole tensors to ranks (sharding by tensor): each tensor is an independent clustering
+    problem (one C per tensor, DESIGN R12), so a rank that holds whole tensors needs no exchange at
+    all -- no count or gamma all-reduce, no replicated table phase.  Longest-processing-time
+    greedy: tensors by size (descending, ties by index) to the least-loaded rank (ties by rank);
+    deterministic, every tensor exactly once.  Returns [rank] -> ascending list of tensor indices."""
+    if world < 1:
+        raise ValueError("bad world")
+    load = [0] * world
+    owned = [[] for _ in range(world)]
+    for t in sorted(range(len(numels)), key=lambda i: (-numels[i], i)):
+        r = min(range(world), key=lambda j: (load[j], j))
+        owned[r].append(t)
+        load[r] += numels[t]
+    return [sorted(o) for o in owned]
 
 
 def allreduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:

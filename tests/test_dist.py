@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 
 from oracle import oracle as O
 from paper_2309_00964_b200 import synth
-from paper_2309_00964_b200.dist import ShardedStep, shard_all, shard_range
+from paper_2309_00964_b200.dist import ShardedStep, assign_tensors, shard_all, shard_range
 
 TAU, T, K = 2e-2, 3, 4
 
@@ -184,6 +184,28 @@ def test_shard_ranges_partition_every_tensor():
             assert all(b - a in (n // world, n // world + 1) for a, b in r)
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5", "ragged"])
+def test_assign_tensors_covers_every_tensor_once_and_balances(cfg):
+    """Sharding by tensor (bench.py's default at N > 1): every tensor on exactly one rank,
+    deterministic, and the largest rank load within one tensor of the mean (the longest-first
+    greedy's bound: a rank only receives a tensor while it is the least loaded)."""
+    if cfg == "ragged":
+        numels = [0, 1, 17, 5_000_000, 3, 131_072_000, 2, 45_088_768] * 5
+    else:
+        numels = [r * c for _, r, c in synth.workload(cfg).shapes]
+    for world in (1, 2, 3, 4, 8):
+        owned = assign_tensors(numels, world)
+        assert owned == assign_tensors(numels, world)
+        flat = sorted(t for o in owned for t in o)
+        assert flat == list(range(len(numels)))
+        loads = [sum(numels[t] for t in o) for o in owned]
+        assert max(loads) <= sum(numels) / world + max(numels)
+        if cfg == "cfg3" and world == 8:
+            assert max(loads) <= 1.01 * sum(numels) / world  # LLaMA-7B at N = 8: within 1%
+    with pytest.raises(ValueError):
+        assign_tensors(numels, 0)
 
 
 def test_world_size_2_gloo_matches_single_process_oracle():

@@ -15,6 +15,10 @@ for wl in cfg2 cfg4 cfg4_b2 cfg5; do
 done
 EDKM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
     --master-port 29517 bench.py --gpus 2 --steps 5 > $O/${TAG}_bench_gloo_n2.json 2> $O/${TAG}_bench_gloo_n2.err
+EDKM_SHARD=slice EDKM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29518 bench.py --gpus 2 --steps 5 --no-e2e > $O/${TAG}_bench_gloo_n2_slice.json \
+    2> $O/${TAG}_bench_gloo_n2_slice.err
+python tools/rank_sim.py --workload cfg3 > $O/${TAG}_rank_sim_cfg3.jsonl 2>/dev/null
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     -k "$K" --log-file $O/${TAG}_launches_bench.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
     --no-graph > /dev/null 2>&1
