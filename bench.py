@@ -289,7 +289,7 @@ def main():
     wl = synth.workload(args.workload)
     p = E.Params(wl.wdtype, wl.bits, wl.tau, wl.max_iter, wl.eps)
 
-    # ---- synthetic inputs, resident in HBM (this rank's slice of every tensor)
+    # ---- synthetic inputs, resident in HBM (this rank's whole tensors, or its slice of every tensor)
     # Sharding at N > 1 (EDKM_SHARD): "tensor" (default while the largest tensor fits a rank's share):
     # whole tensors per rank (dist.assign_tensors, longest-first greedy), independent clustering
     # problems (one C per tensor, R12), so the step has no data-path exchange and no replicated table
