@@ -335,8 +335,8 @@ def main():
 
     # N > 1 collectives: by default on libedkm.so's own NCCL communicator (edkm.Comm, SURVEY S8(b):
     # edkm_comm_allreduce / _allgather on the step's stream); EDKM_COMM=torch uses torch.distributed
-    comm = None
-    if distributed and backend == "nccl" and os.environ.get("EDKM_COMM", "lib") == "lib":
+    comm = None  # (by tensor there is no data-path collective: torch.distributed times the step)
+    if distributed and backend == "nccl" and not tensor_mode and os.environ.get("EDKM_COMM", "lib") == "lib":
         try:
             comm = E.Comm()
         except Exception as e:  # every rank fails alike (same library, same NCCL): torch's NCCL instead
