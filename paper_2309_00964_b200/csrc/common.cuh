@@ -22,6 +22,16 @@ constexpr int kMagPages = 128;
 
 enum WDtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kU8 = 3 };
 
+// Bounds checks of shared- and global-memory indexing, compiled in only for a checking build
+// (-DEDKM_BOUNDS, tools/bounds_check.sh): a failed check is a device assert.  The pool's
+// compute-sanitizer is closed since the round-2 table changes; this is the substitute.
+#ifdef EDKM_BOUNDS
+#include <cassert>
+#define EDKM_BCHECK(c) assert(c)
+#else
+#define EDKM_BCHECK(c) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- decoding
 // Exact value of a 16-bit pattern ("16bit (e.g., BF16 or FP16)").
 __device__ __forceinline__ double decode16(uint32_t u, int wdtype) {

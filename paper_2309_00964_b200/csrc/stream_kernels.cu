@@ -520,8 +520,13 @@ struct F2Policy {
       uint16_t* tab = reinterpret_cast<uint16_t*>(sm);
       const uint8_t* ix = F.idx8 + (int64_t)T * kPatterns;
       const float* C = F.C + (int64_t)T * F.k;
-      for (int u = threadIdx.x; u < kPatterns; u += blockDim.x)
-        tab[u] = pattern_finite(u, A.wdtype) ? round16f(__ldg(C + ix[u]), A.wdtype) : nan16(A.wdtype);
+      for (int u = threadIdx.x; u < kPatterns; u += blockDim.x) {
+        // index entries of absent finite patterns are not written by TF (never read for the output):
+        // clamp before the centroid load so that a stale byte cannot index past C
+        const uint32_t j = ix[u];
+        tab[u] = pattern_finite(u, A.wdtype) && j < (uint32_t)F.k ? round16f(__ldg(C + j), A.wdtype)
+                                                                   : nan16(A.wdtype);
+      }
     } else if (MODE == 2) {
       pbase = F.state[T].win[2];  // chosen once per tensor by TF (table_windows)
       np = F.state[T].win[3];

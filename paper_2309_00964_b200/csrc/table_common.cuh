@@ -11,15 +11,6 @@
 #include "common.cuh"
 #include "launch.h"
 
-// Bounds checks of the table kernels' shared- and global-memory indexing, compiled in only for a
-// checking build (-DEDKM_BOUNDS, tools/bounds_check.sh): a failed check is a device assert.  The
-// pool's compute-sanitizer is closed since the round-2 table changes; this is the substitute.
-#ifdef EDKM_BOUNDS
-#include <cassert>
-#define EDKM_BCHECK(c) assert(c)
-#else
-#define EDKM_BCHECK(c) ((void)0)
-#endif
 
 namespace edkm {
 

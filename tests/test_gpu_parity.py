@@ -334,6 +334,42 @@ def test_rows_beyond_the_shared_stage(dtype, bits, lo, hi, n):
     assert beyond == nt  # every tensor has rows beyond its CTAs' stages
 
 
+@pytest.mark.parametrize("dtype,bits", [(torch.bfloat16, 3), (torch.float16, 4), (torch.bfloat16, 6)])
+def test_absent_pattern_entries_are_never_read(dtype, bits):
+    """TF writes the W~ tables (fp32, 16-bit, hard index) only for populated and non-finite
+    patterns (include/edkm.h); every output must come out bit-identical whatever the other entries
+    hold: one plan's saved/table/workspace buffers start as 0xFF bytes (stale index bytes past k),
+    the other's as zeros; soft (16-bit and fp32), hard-value and hard-index outputs and dW compared."""
+    n = 300_001
+    W = synth.normal_tensor(n, 0.02, dtype, 61)
+    W[[3, 99]] = torch.tensor([float("nan"), -float("inf")], dtype=dtype)
+    G = synth.normal_tensor(n, 1e-3, dtype, 62).cuda()
+    Wd = W.cuda()
+    p = E.Params(dtype, bits, 1e-5, 4)
+    C0 = torch.tensor([synth.quantile_centroids(1 << bits, 0.02)], dtype=torch.float32, device="cuda")
+    res = []
+    for fill in (0xFF, 0x00):
+        plan = E.Plan([n], p, "cuda")
+        for buf in (plan.saved, plan.ws, plan.table.view(torch.uint8)):
+            buf.fill_(fill)
+        outs = {}
+        for odt in (dtype, torch.float32):
+            wt = torch.empty(n, dtype=odt, device="cuda")
+            dw = torch.empty(n, dtype=odt, device="cuda")
+            plan.step([Wd], [G], C0, [wt], [dw])
+            outs[f"soft_{odt}"], outs[f"dw_{odt}"] = wt.cpu(), dw.cpu()
+        hv = torch.empty(n, dtype=dtype, device="cuda")
+        plan.reconstruct([Wd], [hv], E.HARD_VALUE)
+        hi = torch.empty(n, dtype=torch.uint8, device="cuda")
+        plan.reconstruct([Wd], [hi], E.HARD_INDEX)
+        torch.cuda.synchronize()
+        outs["hard_value"], outs["hard_index"] = hv.cpu(), hi.cpu()
+        res.append(outs)
+    for k in res[0]:
+        a, b = res[0][k], res[1][k]
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8)), k
+
+
 def test_many_ragged_tensors_and_empty():
     sizes = [0, 1, 17, 4097, 65536 * 3 + 5, 0, 250_001, 2, 31, 33]
     p = E.Params(torch.bfloat16, 3, 1e-3, 4)
